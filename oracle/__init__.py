@@ -1,0 +1,179 @@
+"""CPU oracle of the GenVectorX hot path (arXiv 2312.02756) — TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+and ``--impl reference`` legs may import this package. The product path
+(``paper_2312_02756_b200``) never imports it and shares no code with it.
+
+The arithmetic lives in plain C (``gvx_oracle.c`` / ``gvx_oracle_body.inc``),
+compiled by gcc ``-O2 -ffp-contract=off`` against glibc libm into
+``liboracle.so``; this module only marshals numpy arrays through ctypes.
+Each function cites the PAPER.md / SPEC.md passage its C body follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_SOURCES = ["gvx_oracle.c", "gvx_oracle_body.inc", "gvx_oracle.h"]
+
+PTETAPHIM = 0
+PXPYPZE = 1
+_COORDS = {"ptetaphim": PTETAPHIM, "pxpypze": PXPYPZE}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C, no FMA contraction)."""
+    src_mtime = max(os.path.getmtime(os.path.join(_HERE, s)) for s in _SOURCES)
+    if not force and os.path.exists(_LIB_PATH) and os.path.getmtime(_LIB_PATH) >= src_mtime:
+        return _LIB_PATH
+    cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC", "-shared",
+           "-Wall", "-Wextra", "-o", _LIB_PATH + ".tmp", os.path.join(_HERE, "gvx_oracle.c"), "-lm"]
+    subprocess.run(cmd, check=True)
+    os.replace(_LIB_PATH + ".tmp", _LIB_PATH)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        I64 = ctypes.c_int64
+        for sfx, T in (("f32", ctypes.c_float), ("f64", ctypes.c_double)):
+            getattr(lib, f"gvx_ref_invariant_mass_{sfx}").argtypes = [ctypes.c_int, P, P, I64, P, P]
+            getattr(lib, f"gvx_ref_boost_{sfx}").argtypes = [P, P, I64, P, P]
+            f = getattr(lib, f"gvx_ref_boost_uniform_{sfx}")
+            f.argtypes = [P, T, T, T, I64, P]
+            f.restype = ctypes.c_int
+            getattr(lib, f"gvx_ref_cm_mass_{sfx}").argtypes = [ctypes.c_int, P, P, I64, P, P, P]
+            getattr(lib, f"gvx_ref_mass_histogram_{sfx}").argtypes = [
+                ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                ctypes.c_int, P, P]
+        lib.gvx_ref_find_bin.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_int32]
+        lib.gvx_ref_find_bin.restype = ctypes.c_int32
+        _lib = lib
+    return _lib
+
+
+def _sfx(dtype) -> str:
+    dtype = np.dtype(dtype)
+    if dtype == np.float32:
+        return "f32"
+    if dtype == np.float64:
+        return "f64"
+    raise TypeError(f"oracle supports float32/float64, got {dtype}")
+
+
+def _vecs(a, ncomp: int, dtype=None) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=dtype)
+    if a.ndim == 1 and a.size == ncomp:
+        a = a.reshape(1, ncomp)
+    if a.ndim != 2 or a.shape[1] != ncomp:
+        raise ValueError(f"expected an [N, {ncomp}] array, got shape {a.shape}")
+    return a
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None else None
+
+
+def invariant_mass(v1, v2, coords: str = "ptetaphim"):
+    """InvariantMasses, PAPER.md:141-151 (Fig. 1): ``m[i] = (v1[i] + v2[i]).mass()``.
+
+    Returns ``(M, E_lab)``, both of v1's dtype; ``E_lab = E1 + E2`` is the
+    tolerance scale (reading R5).
+    """
+    v1 = _vecs(v1, 4)
+    v2 = _vecs(v2, 4, v1.dtype)
+    if v1.shape != v2.shape:
+        raise ValueError(f"length mismatch: {v1.shape[0]} vs {v2.shape[0]}")
+    n = v1.shape[0]
+    m = np.empty(n, v1.dtype)
+    e = np.empty(n, v1.dtype)
+    getattr(_load(), f"gvx_ref_invariant_mass_{_sfx(v1.dtype)}")(
+        _COORDS[coords], _ptr(v1), _ptr(v2), n, _ptr(m), _ptr(e))
+    return m, e
+
+
+def boost(v, beta):
+    """Per-event Lorentz boost, PAPER.md:136 / SPEC.md:188-200.
+
+    ``v`` is [N, 4] PxPyPzE, ``beta`` [N, 3]. Returns ``(out, S)`` with
+    ``S = γ(E + |β||p|)`` the tolerance scale (reading R5); |β| ≥ 1 → NaN×4.
+    """
+    v = _vecs(v, 4)
+    beta = _vecs(beta, 3, v.dtype)
+    if v.shape[0] != beta.shape[0]:
+        raise ValueError(f"length mismatch: {v.shape[0]} vs {beta.shape[0]}")
+    n = v.shape[0]
+    out = np.empty_like(v)
+    s = np.empty(n, v.dtype)
+    getattr(_load(), f"gvx_ref_boost_{_sfx(v.dtype)}")(_ptr(v), _ptr(beta), n, _ptr(out), _ptr(s))
+    return out, s
+
+
+class DomainError(ValueError):
+    pass
+
+
+def boost_uniform(v, bx, by, bz):
+    """The paper's single-matrix ApplyBoost; |β| ≥ 1 raises DomainError
+    (SPEC.md:191)."""
+    v = _vecs(v, 4)
+    n = v.shape[0]
+    out = np.empty_like(v)
+    rc = getattr(_load(), f"gvx_ref_boost_uniform_{_sfx(v.dtype)}")(_ptr(v), bx, by, bz, n, _ptr(out))
+    if rc != 0:
+        raise DomainError(f"|beta|^2 = {bx*bx + by*by + bz*bz} >= 1")
+    return out
+
+
+def cm_mass(v1, v2, coords: str = "ptetaphim", want_boosted: bool = False):
+    """Boost each pair to its CM frame (β = −P/E), then the signed mass (reading R11).
+
+    Returns ``(M_cm, E_lab[, boosted])``; boosted is [N, 8] (vector 1, vector 2).
+    """
+    v1 = _vecs(v1, 4)
+    v2 = _vecs(v2, 4, v1.dtype)
+    if v1.shape != v2.shape:
+        raise ValueError(f"length mismatch: {v1.shape[0]} vs {v2.shape[0]}")
+    n = v1.shape[0]
+    m = np.empty(n, v1.dtype)
+    e = np.empty(n, v1.dtype)
+    bo = np.empty((n, 8), v1.dtype) if want_boosted else None
+    getattr(_load(), f"gvx_ref_cm_mass_{_sfx(v1.dtype)}")(
+        _COORDS[coords], _ptr(v1), _ptr(v2), n, _ptr(m), _ptr(e), _ptr(bo))
+    return (m, e, bo) if want_boosted else (m, e)
+
+
+def mass_histogram(v1, v2, lo: float, hi: float, nbins: int, cm: bool = False,
+                   coords: str = "ptetaphim", bins=None):
+    """Fused mass histogram (north_star; reading R12). Returns ``(bins uint64[nbins+2], M)``.
+
+    ``bins`` accumulates if given (the caller's zeroed array)."""
+    v1 = _vecs(v1, 4)
+    v2 = _vecs(v2, 4, v1.dtype)
+    if v1.shape != v2.shape:
+        raise ValueError(f"length mismatch: {v1.shape[0]} vs {v2.shape[0]}")
+    n = v1.shape[0]
+    if bins is None:
+        bins = np.zeros(nbins + 2, np.uint64)
+    assert bins.dtype == np.uint64 and bins.shape == (nbins + 2,) and bins.flags.c_contiguous
+    m = np.empty(n, v1.dtype)
+    getattr(_load(), f"gvx_ref_mass_histogram_{_sfx(v1.dtype)}")(
+        _COORDS[coords], _ptr(v1), _ptr(v2), n, lo, hi, nbins, int(bool(cm)), _ptr(bins), _ptr(m))
+    return bins, m
+
+
+def find_bin(x: float, lo: float, hi: float, nbins: int) -> int:
+    """ROOT FindFixBin in double (reading R12)."""
+    return int(_load().gvx_ref_find_bin(float(x), float(lo), float(hi), int(nbins)))

@@ -1,0 +1,418 @@
+"""Pins for the CPU oracle (oracle/) against things other than itself.
+
+Each test checks the oracle against what the paper/SPEC and mathematics fix:
+the SPEC's printed worked examples (tests/golden/spec_examples.json), closed
+forms named in BASELINE.json's north_star, invariants (Lorentz invariance,
+metric preservation, β then −β), 40-digit mpmath truth computed along a
+DIFFERENT algebraic route than the oracle's (so a dropped term, a wrong sign,
+a swapped sin/cos or a transposed index fails), and exact rational brute force
+for the histogram binning. No expected value here comes from the CUDA path.
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")
+MMU = synth.MUON_MASS
+mp.mp.dps = 40
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def O(oracle_lib):
+    return oracle_lib
+
+
+# --------------------------------------------------------------------------
+# High-precision truth along an independent route
+# --------------------------------------------------------------------------
+
+def truth_mass2_ptetaphim(a, b):
+    """M² and E_lab from the rapidity-angle form (not the oracle's Cartesian sum):
+    M² = m1|m1| + m2|m2| + 2(E1E2 − pt1pt2(cos(φ1−φ2) + sinh η1 sinh η2)),
+    E_i = sqrt(m_i|m_i| + pt_i² cosh² η_i); valid when no E² clamp applies."""
+    pt1, e1, f1, m1 = (mp.mpf(float(x)) for x in a)
+    pt2, e2, f2, m2 = (mp.mpf(float(x)) for x in b)
+    E1 = mp.sqrt(m1 * abs(m1) + (pt1 * mp.cosh(e1)) ** 2)
+    E2 = mp.sqrt(m2 * abs(m2) + (pt2 * mp.cosh(e2)) ** 2)
+    M2 = m1 * abs(m1) + m2 * abs(m2) + 2 * (E1 * E2 - pt1 * pt2 * (mp.cos(f1 - f2) + mp.sinh(e1) * mp.sinh(e2)))
+    return M2, E1 + E2
+
+
+def truth_boost(v, beta):
+    """Boost by rapidity ζ = atanh|β| along n = β/|β| (a different route than Λ):
+    E' = cosh ζ E + sinh ζ p∥,  p' = p + ((cosh ζ − 1) p∥ + sinh ζ E) n."""
+    px, py, pz, E = (mp.mpf(float(x)) for x in v)
+    bx, by, bz = (mp.mpf(float(x)) for x in beta)
+    b = mp.sqrt(bx * bx + by * by + bz * bz)
+    if b == 0:
+        return [px, py, pz, E]
+    nx, ny, nz = bx / b, by / b, bz / b
+    z = mp.atanh(b)
+    ppar = px * nx + py * ny + pz * nz
+    k = (mp.cosh(z) - 1) * ppar + mp.sinh(z) * E
+    return [px + k * nx, py + k * ny, pz + k * nz, mp.cosh(z) * E + mp.sinh(z) * ppar]
+
+
+def signed_sq(x):
+    return x * abs(x)
+
+
+# --------------------------------------------------------------------------
+# SPEC worked examples (golden)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_golden_conversion_at_rest(O, golden, dt):
+    for ex in golden["conversion_ptetaphim_to_pxpypze"]:
+        # single vector paired with the zero vector: E_lab = E, M = m
+        m, e = O.invariant_mass(np.array([ex["in"]], dt), np.zeros((1, 4), dt))
+        assert e[0] == ex["out"][3], ex["cite"]
+        assert m[0] == ex["in"][3], ex["cite"]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_golden_mass_pxpypze(O, golden, dt):
+    z = np.zeros((1, 4), dt)
+    for ex in golden["mass_pxpypze"]:
+        m, _ = O.invariant_mass(np.array([ex["v"]], dt), z, coords="pxpypze")
+        if "mass" in ex:
+            assert m[0] == ex["mass"], ex["cite"]
+        else:
+            assert m[0] == dt(math.sqrt(ex["mass_squared"])), ex["cite"]
+    for ex in golden["batch_mass_pxpypze"] + golden["add_pxpypze"]:
+        a = np.array([ex.get("v1", ex.get("a"))] * 7, dt)
+        b = np.array([ex.get("v2", ex.get("b"))] * 7, dt)
+        m, e = O.invariant_mass(a, b, coords="pxpypze")
+        if "mass" in ex:
+            assert np.all(m == ex["mass"]), ex["cite"]
+        elif "mass_squared" in ex:
+            assert np.all(m == dt(math.sqrt(ex["mass_squared"]))), ex["cite"]
+        else:  # additive examples: check through the sum's energy and mass
+            s = ex["sum"]
+            assert np.all(e == s[3]), ex["cite"]
+            exp_m2 = s[3] ** 2 - (s[0] ** 2 + s[1] ** 2 + s[2] ** 2)
+            assert np.allclose(m * np.abs(m), exp_m2, rtol=1e-6 if dt == np.float32 else 1e-15)
+
+
+def test_golden_batch_empty(O, golden):
+    for dt in (np.float32, np.float64):
+        m, e = O.invariant_mass(np.zeros((0, 4), dt), np.zeros((0, 4), dt))
+        assert m.shape == (0,)
+        out, s = O.boost(np.zeros((0, 4), dt), np.zeros((0, 3), dt))
+        assert out.shape == (0, 4)
+        bins, _ = O.mass_histogram(np.zeros((0, 4), dt), np.zeros((0, 4), dt), 0.25, 300.0, 1000)
+        assert bins.sum() == 0
+
+
+def boost_matrix_from_oracle(O, beta, dt=np.float64):
+    """Columns of Λ = oracle boost applied to the 4 basis vectors."""
+    basis = np.eye(4, dtype=dt)
+    out, _ = O.boost(basis, np.array([beta] * 4, dt))
+    return out.T  # out[j] = Λ e_j = column j
+
+
+def test_golden_boost_matrix(O, golden):
+    for ex in golden["boost_matrix"]:
+        L = boost_matrix_from_oracle(O, ex["beta"])
+        if ex.get("identity"):
+            assert np.array_equal(L, np.eye(4)), ex["cite"]
+            continue
+        assert L[2, 2] == pytest.approx(ex["L_zz"], abs=1e-15), ex["cite"]
+        assert L[2, 3] == pytest.approx(ex["L_zt"], abs=1e-15), ex["cite"]
+        assert L[3, 2] == pytest.approx(ex["L_tz"], abs=1e-15), ex["cite"]
+        assert L[3, 3] == pytest.approx(ex["L_tt"], abs=1e-15), ex["cite"]
+        assert L[0, 0] == ex["L_xx"] and L[1, 1] == ex["L_yy"], ex["cite"]
+        assert L[0, 1] == 0 and L[0, 3] == 0 and L[1, 3] == 0
+
+
+def test_golden_boost_apply(O, golden):
+    for ex in golden["boost_apply"]:
+        m = ex["rest_mass"]
+        for dt, tol in ((np.float64, 1e-15), (np.float32, 1e-6)):
+            out, _ = O.boost(np.array([[0, 0, 0, m]], dt), np.array([ex["beta"]], dt))
+            assert np.allclose(out[0], np.array(ex["out_over_m"]) * m, rtol=tol, atol=tol), ex["cite"]
+
+
+def test_golden_boost_domain(O, golden):
+    for ex in golden["boost_domain_error"]:
+        with pytest.raises(O.DomainError):
+            O.boost_uniform(np.zeros((3, 4)), *ex["beta"])
+        out, s = O.boost(np.ones((1, 4)), np.array([ex["beta"]]))
+        assert np.all(np.isnan(out)) and np.isnan(s[0]), ex["cite"]
+    # |β| = 1 exactly is also rejected (b2 < 1 is required)
+    out, _ = O.boost(np.ones((1, 4)), np.array([[0.0, 0.0, 1.0]]))
+    assert np.all(np.isnan(out))
+
+
+# --------------------------------------------------------------------------
+# Closed forms from the north star
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_single_vector_mass_is_m(O, dt):
+    rng = np.random.default_rng(1)
+    v = np.stack([rng.uniform(1, 100, 200), rng.uniform(-2.5, 2.5, 200), rng.uniform(-np.pi, np.pi, 200),
+                  rng.uniform(0.1, 90, 200)], axis=1).astype(dt)
+    m, e = O.invariant_mass(v, np.zeros_like(v))
+    # |M² − m²| ≤ τ·E² (τ = the north-star tolerance of the dtype)
+    tau = 1e-12 if dt == np.float64 else 1e-5
+    assert np.all(np.abs(signed_sq(m.astype(np.float64)) - signed_sq(v[:, 3].astype(np.float64)))
+                  <= tau * e.astype(np.float64) ** 2)
+    # spacelike sign convention: pt = 1, m = −0.5 → −0.5
+    m, _ = O.invariant_mass(np.array([[1.0, 0.0, 0.0, -0.5]], dt), np.zeros((1, 4), dt))
+    assert m[0] < 0 and m[0] == pytest.approx(-0.5, rel=4 * np.finfo(dt).eps)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_back_to_back_massless_pair(O, dt):
+    # pt = 25, η = ±1.1, Δφ = π → M = 2·pt·cosh η (north star: "back-to-back massless pairs give M = 2E")
+    a = np.array([[25.0, 1.1, 0.3, 0.0]], dt)
+    b = np.array([[25.0, -1.1, 0.3 - math.pi, 0.0]], dt)
+    m, e = O.invariant_mass(a, b)
+    exact = 2 * 25 * mp.cosh(mp.mpf(float(dt(1.1))))
+    tau = 1e-12 if dt == np.float64 else 1e-5
+    assert abs(mp.mpf(float(m[0])) ** 2 - exact ** 2) <= tau * exact ** 2
+    assert float(exact) == pytest.approx(83.425927691112816634, rel=1e-15 if dt == np.float64 else 1e-6)
+
+
+def test_v_plus_v_is_twice_m(O):
+    # PtEtaPhiM(3, 0.5, 1.0, 1) + itself → mass 2
+    v = np.array([[3.0, 0.5, 1.0, 1.0]])
+    m, _ = O.invariant_mass(v, v)
+    assert m[0] == pytest.approx(2.0, abs=1e-14)
+
+
+def test_spec_conversion_example_mpmath(O):
+    # (10, 1.2, 0.5, 0.105) → E = sqrt(0.105² + 10² cosh² 1.2); M of (v, 0) = 0.105
+    v = np.array([[10.0, 1.2, 0.5, 0.105]])
+    m, e = O.invariant_mass(v, np.zeros_like(v))
+    E = mp.sqrt(mp.mpf(0.105) ** 2 + 100 * mp.cosh(mp.mpf(1.2)) ** 2)
+    assert abs(e[0] - E) <= 4e-16 * E
+    assert float(E) == pytest.approx(18.106860118426809386, rel=1e-16)
+    # the Cartesian image: boosting by β = 0 and reading back through the pxpypze mass path
+    px, py, pz = 10 * mp.cos(0.5), 10 * mp.sin(0.5), 10 * mp.sinh(1.2)
+    assert float(px) == pytest.approx(8.7758256189037271612, rel=1e-16)
+    assert float(pz) == pytest.approx(15.09461355412172616, rel=1e-16)
+    mc, ec = O.invariant_mass(np.array([[float(px), float(py), float(pz), float(E)]]), np.zeros((1, 4)),
+                              coords="pxpypze")
+    assert ec[0] == pytest.approx(e[0], rel=1e-16)
+    assert abs(mc[0] ** 2 - m[0] ** 2) <= 1e-12 * E ** 2
+
+
+def test_dimuon_pins(O):
+    a = np.array([[45.0, 0.3, 0.1, MMU]])
+    b = np.array([[40.0, -0.8, 2.9, MMU]])
+    m, e = O.invariant_mass(a, b)
+    assert m[0] == pytest.approx(96.946954876884514685, rel=1e-14)
+    assert e[0] == pytest.approx(100.53785398749637737, rel=1e-15)
+    # near-collinear pair (cancellation regime, M/E = 1.6e-3)
+    a = np.array([[20.0, 2.4, -3.0, MMU]])
+    b = np.array([[20.0, 2.39, -3.01, MMU]])
+    m, e = O.invariant_mass(a, b)
+    M2t, Et = truth_mass2_ptetaphim(a[0], b[0])
+    assert float(mp.sqrt(M2t)) == pytest.approx(0.35306635229398653897, rel=1e-15)
+    assert abs(m[0] ** 2 - M2t) <= 1e-14 * Et ** 2
+
+
+# --------------------------------------------------------------------------
+# Random events against 40-digit truth along the rapidity route
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt,bound", [(np.float64, 1e-14), (np.float32, 2e-6)])
+def test_mass_random_vs_mpmath(O, dt, bound):
+    v1, v2 = synth.muon_pairs(np.arange(400), seed=7, dtype=dt)
+    # add heavier, wider-η and spacelike-free variety
+    rng = np.random.default_rng(3)
+    extra1 = np.stack([rng.uniform(0.5, 500, 100), rng.uniform(-5, 5, 100), rng.uniform(-20, 20, 100),
+                       rng.uniform(0, 100, 100)], 1).astype(dt)
+    extra2 = np.stack([rng.uniform(0.5, 500, 100), rng.uniform(-5, 5, 100), rng.uniform(-20, 20, 100),
+                       rng.uniform(0, 100, 100)], 1).astype(dt)
+    v1 = np.concatenate([v1, extra1])
+    v2 = np.concatenate([v2, extra2])
+    m, e = O.invariant_mass(v1, v2)
+    worst = 0.0
+    for i in range(len(m)):
+        M2t, Et = truth_mass2_ptetaphim(v1[i], v2[i])
+        err = abs(signed_sq(mp.mpf(float(m[i]))) - M2t) / Et ** 2
+        worst = max(worst, float(err))
+        assert abs(mp.mpf(float(e[i])) - Et) <= 4 * np.finfo(dt).eps * Et
+    assert worst <= bound, worst
+
+
+@pytest.mark.parametrize("dt,bound", [(np.float64, 1e-14), (np.float32, 1e-5)])
+def test_boost_random_vs_rapidity_truth(O, dt, bound):
+    v, beta = synth.boost_inputs(np.arange(300), seed=11, dtype=dt)
+    out, s = O.boost(v, beta)
+    worst = 0.0
+    for i in range(len(v)):
+        t = truth_boost(v[i], beta[i])
+        S = float(s[i])
+        for c in range(4):
+            worst = max(worst, float(abs(mp.mpf(float(out[i, c])) - t[c])) / S)
+    assert worst <= bound, worst
+
+
+def test_boost_metric_preservation(O):
+    # Λᵀ g Λ = g, g = diag(−1, −1, −1, +1)
+    g = np.diag([-1.0, -1.0, -1.0, 1.0])
+    _, beta = synth.boost_inputs(np.arange(200), seed=5)
+    for b in beta:
+        L = boost_matrix_from_oracle(O, b)
+        assert np.max(np.abs(L.T @ g @ L - g)) <= 1e-12
+        assert np.allclose(L, L.T, atol=0)  # a pure boost is symmetric
+
+
+def test_boost_inverse_and_invariance(O):
+    v, beta = synth.boost_inputs(np.arange(2000), seed=9)
+    out, s = O.boost(v, beta)
+    back, _ = O.boost(out, -beta)
+    assert np.max(np.abs(back - v) / s[:, None]) <= 1e-13  # β then −β = identity
+    m0, _ = O.invariant_mass(v, np.zeros_like(v), coords="pxpypze")
+    m1, _ = O.invariant_mass(out, np.zeros_like(out), coords="pxpypze")
+    assert np.max(np.abs(signed_sq(m1) - signed_sq(m0)) / s ** 2) <= 1e-13  # M invariant under boosts
+    # rest particle → E = γm, |p| = γβm (north star), β = (0.3, −0.4, 0.5)
+    out, _ = O.boost(np.array([[0.0, 0.0, 0.0, 1.0]]), np.array([[0.3, -0.4, 0.5]]))
+    g = 1 / mp.sqrt(1 - mp.mpf(0.3) ** 2 - mp.mpf(0.4) ** 2 - mp.mpf(0.5) ** 2)
+    assert out[0, 3] == pytest.approx(float(g), rel=2e-16)
+    assert float(g) == pytest.approx(1.4142135623730950645, rel=1e-16)
+    assert math.sqrt(out[0, 0] ** 2 + out[0, 1] ** 2 + out[0, 2] ** 2) == pytest.approx(1.0000000000000000222, rel=4e-16)
+    assert out[0, 0] == pytest.approx(0.3 * float(g), rel=4e-16)
+    assert out[0, 1] == pytest.approx(-0.4 * float(g), rel=4e-16)
+
+
+def test_boost_uniform_equals_per_event(O):
+    v, _ = synth.boost_inputs(np.arange(50), seed=2)
+    b = (0.1, 0.2, -0.3)
+    u = O.boost_uniform(v, *b)
+    p, _ = O.boost(v, np.array([b] * 50))
+    assert np.array_equal(u, p)
+
+
+# --------------------------------------------------------------------------
+# CM boost (reading R11)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_cm_mass_invariance_and_rest_frame(O, dt):
+    v1, v2 = synth.muon_pairs(np.arange(3000), seed=21, dtype=dt)
+    mcm, e, bo = O.cm_mass(v1, v2, want_boosted=True)
+    mlab, _ = O.invariant_mass(v1, v2)
+    ok = np.isfinite(mcm)
+    if dt == np.float64:
+        assert ok.all()
+        tau = 1e-12
+    else:
+        tau = 1e-5
+    e = e.astype(np.float64)
+    assert np.all(np.abs(signed_sq(mcm[ok].astype(np.float64)) - signed_sq(mlab[ok].astype(np.float64)))
+                  <= tau * e[ok] ** 2)
+    if dt == np.float64:
+        P = bo[:, 0:3] + bo[:, 4:7]
+        E = bo[:, 3] + bo[:, 7]
+        S = e ** 2 / np.maximum(mlab, 1e-300)  # γ·E scale of the CM boost
+        assert np.max(np.abs(P).max(1) / S) <= 1e-14  # total momentum vanishes
+        assert np.max(np.abs(E - mlab) / S) <= 1e-14  # E' = M
+    # dimuon pin: E' = M
+    m, _, bo = O.cm_mass(np.array([[45.0, 0.3, 0.1, MMU]]), np.array([[40.0, -0.8, 2.9, MMU]]), want_boosted=True)
+    assert m[0] == pytest.approx(96.946954876884514685, rel=1e-13)
+    assert bo[0, 3] + bo[0, 7] == pytest.approx(96.946954876884514685, rel=1e-13)
+
+
+def test_cm_degenerate(O):
+    # already at rest in the CM: β = 0 → boosted = input
+    a = np.array([[3.0, 4.0, 5.0, 13.0]])
+    b = np.array([[-3.0, -4.0, -5.0, 13.0]])
+    m, _, bo = O.cm_mass(a, b, coords="pxpypze", want_boosted=True)
+    assert m[0] == 26.0 and np.array_equal(bo[0], np.concatenate([a[0], b[0]]))
+    # zero-energy pair → NaN (reading R11) → overflow bin
+    z = np.zeros((1, 4))
+    m, _ = O.cm_mass(z, z)
+    assert np.isnan(m[0])
+    bins, _ = O.mass_histogram(z, z, 0.25, 300.0, 1000, cm=True)
+    assert bins[1001] == 1 and bins.sum() == 1
+    # lightlike collinear pair: β² = 1 → NaN
+    a = np.array([[0.0, 0.0, 5.0, 5.0]])
+    m, _ = O.cm_mass(a, a, coords="pxpypze")
+    assert np.isnan(m[0])
+
+
+# --------------------------------------------------------------------------
+# Histogram binning vs exact rational brute force
+# --------------------------------------------------------------------------
+
+def brute_bin(x, lo, hi, nbins):
+    """Scan the edges lo + b·(hi−lo)/nbins exactly (rationals)."""
+    if math.isnan(x):
+        return nbins + 1
+    if math.isinf(x):
+        return 0 if x < 0 else nbins + 1
+    X, L, H = Fraction(x), Fraction(lo), Fraction(hi)
+    if X < L:
+        return 0
+    if X >= H:
+        return nbins + 1
+    w = (H - L) / nbins
+    for b in range(1, nbins + 1):
+        if L + (b - 1) * w <= X < L + b * w:
+            return b
+    raise AssertionError
+
+
+def test_find_bin_vs_brute_force(O):
+    lo, hi, nb = 0.25, 300.0, 1000
+    rng = np.random.default_rng(0)
+    xs = list(rng.uniform(lo - 20, hi + 20, 3000)) + [lo, hi, -0.0, 0.0, float("nan"), float("inf"),
+                                                      -float("inf"), np.nextafter(lo, -1), np.nextafter(hi, -1)]
+    w = (hi - lo) / nb
+    for x in xs:
+        b_or = O.find_bin(x, lo, hi, nb)
+        b_bf = brute_bin(x, lo, hi, nb)
+        # the only allowed disagreement: within float tolerance of an interior edge
+        near_edge = (lo <= x < hi) and abs((x - lo) / w - round((x - lo) / w)) < 1e-9
+        assert b_or == b_bf or near_edge, (x, b_or, b_bf)
+    assert O.find_bin(float("nan"), lo, hi, nb) == nb + 1
+    assert O.find_bin(hi, lo, hi, nb) == nb + 1
+    assert O.find_bin(lo, lo, hi, nb) == 1
+    assert O.find_bin(-0.0, 0.0, 1.0, 10) == 1
+    assert O.find_bin(0.15, 0.0, 1.0, 10) == brute_bin(0.15, 0.0, 1.0, 10)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("cm", [False, True])
+def test_histogram_is_bincount_of_masses(O, dt, cm):
+    v1, v2 = synth.muon_pairs(np.arange(5000), seed=4, dtype=dt)
+    bins, m = O.mass_histogram(v1, v2, 0.25, 300.0, 1000, cm=cm)
+    assert bins.sum() == 5000
+    ref = np.zeros(1002, np.uint64)
+    for x in m:
+        ref[brute_bin(float(x), 0.25, 300.0, 1000)] += 1
+    assert np.array_equal(bins, ref)
+    if cm:
+        mm, _ = O.cm_mass(v1, v2)
+    else:
+        mm, _ = O.invariant_mass(v1, v2)
+    assert np.array_equal(m, mm, equal_nan=True)
+    # accumulation: a second call adds
+    O.mass_histogram(v1, v2, 0.25, 300.0, 1000, cm=cm, bins=bins)
+    assert np.array_equal(bins, 2 * ref)
+
+
+def test_histogram_single_bin_stress(O):
+    # every pair has the same mass → all counts in one bin
+    v = np.tile(np.array([[0.0, 0.0, 0.0, 45.5]]), (1000, 1))
+    bins, _ = O.mass_histogram(v, v, 0.25, 300.0, 1000, coords="pxpypze")
+    b = brute_bin(91.0, 0.25, 300.0, 1000)
+    assert bins[b] == 1000 and bins.sum() == 1000
