@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native GenVectorX hot path (arXiv 2312.02756).
+
+One STEP = one pass of every hot-path row of SURVEY.md §8(a) over one batch of
+N synthetic events (N = 1e8 per GPU, BASELINE.json metric "... at N=1e8"):
+  K1 gvx_invariant_mass   N PtEtaPhiM pairs -> N masses
+  K2 gvx_boost            N PxPyPzE vectors by per-event beta -> N vectors
+  K3 gvx_mass_histogram   the N pairs -> 1000-bin mass histogram (lab frame)
+  K3 gvx_mass_histogram   the N pairs, boosted to their CM frame -> histogram
+  (N>1) NCCL all-reduce of both histograms' bins — the path's only exchange.
+value = events processed by all ranks / max-over-ranks step time (weak
+scaling: every rank owns N events of the global index space).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f64|f32]
+       python bench.py --impl reference ...   (the CPU oracle as reference arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "events/sec and achieved HBM GB/s (% of B200 peak) for InvariantMass/Boost at N=1e8"
+UNIT = "events/s"
+LO, HI, NB = 0.25, 300.0, 1000
+# Algorithmic bytes per event, per element size es.
+BYTES = {
+    "invariant_mass": lambda es: 8 * es + es,     # two PtEtaPhiM vectors in, one mass out
+    "boost": lambda es: 4 * es + 3 * es + 4 * es,  # vector + beta in, vector out
+    "mass_histogram": lambda es: 8 * es,           # two vectors in (bins: per-call constant)
+    "mass_histogram_cm": lambda es: 8 * es,
+}
+KERNEL_ORDER = ["invariant_mass", "boost", "mass_histogram", "mass_histogram_cm"]
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--dtype", choices=["f64", "f32"], default="f64")
+    p.add_argument("--n", type=float, default=1e8, help="events per GPU")
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=1 << 21, help="events in the oracle's bounded sample")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy_ read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------
+# the oracle as CPU baseline / reference arm (bounded sample, one thread)
+# ----------------------------------------------------------------------------
+
+def oracle_step_rate(n_sample: int, dtype: str, repeats: int = 3):
+    import numpy as np
+
+    import oracle
+    import synth
+    dt = np.float64 if dtype == "f64" else np.float32
+    idx = np.arange(n_sample)
+    v1, v2 = synth.muon_pairs(idx, dtype=dt)
+    v, b = synth.boost_inputs(idx, dtype=dt)
+    best = float("inf")
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        oracle.invariant_mass(v1, v2)
+        oracle.boost(v, b)
+        oracle.mass_histogram(v1, v2, LO, HI, NB)
+        oracle.mass_histogram(v1, v2, LO, HI, NB, cm=True)
+        best = min(best, time.perf_counter() - t0)
+    return n_sample / best, best
+
+
+def cpu_baseline_obj(n_sample: int, dtype: str):
+    rate, t = oracle_step_rate(n_sample, dtype)
+    return {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n_sample} events of the same synthetic workload ({dtype}), one full step "
+                      f"(mass + boost + lab histogram + CM histogram), single-threaded C oracle "
+                      f"(gcc -O2 -ffp-contract=off), best of 3 ({t:.2f} s)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_sample = args.cpu_sample
+    times = []
+    import numpy as np
+
+    import oracle
+    import synth
+    dt = np.float64 if args.dtype == "f64" else np.float32
+    idx = np.arange(n_sample)
+    v1, v2 = synth.muon_pairs(idx, dtype=dt)
+    v, b = synth.boost_inputs(idx, dtype=dt)
+
+    def step():
+        oracle.invariant_mass(v1, v2)
+        oracle.boost(v, b)
+        oracle.mass_histogram(v1, v2, LO, HI, NB)
+        oracle.mass_histogram(v1, v2, LO, HI, NB, cm=True)
+
+    for _ in range(args.warmup):
+        step()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = n_sample / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (synth/, seed 12345)",
+        "config": config_obj(args, world=args.gpus, ref_sample=n_sample),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{n_sample} events per step (bounded sample of the workload), single thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_obj(args, world, ref_sample=None):
+    n = int(args.n)
+    es = 8 if args.dtype == "f64" else 4
+    in_bytes = n * (8 * es + 7 * es)
+    c = {"workload": f"GenVectorX hot path step: mass + per-event boost + lab & CM 1000-bin histograms, "
+                     f"N={n:.0e} events per GPU ({args.dtype}, PtEtaPhiM/PxPyPzE AoS)",
+         "n_events_per_gpu": n, "global_events": n * world, "layout": "AoS",
+         "hist": {"lo": LO, "hi": HI, "nbins": NB},
+         "l2": f"inputs larger than L2 ({in_bytes / 1e9:.1f} GB per GPU >> 126 MB), no flush needed",
+         "parallelism": f"dp{world} (event-index shards, NCCL bin all-reduce)"}
+    if ref_sample:
+        c["reference_sample_events"] = ref_sample
+    return c
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md recipe)
+# ----------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.out = out
+        else:
+            self.out = ""
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        loaded = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_02756_b200 as gvx
+    import synth.device as sd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = int(args.n)
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    es = 8 if args.dtype == "f64" else 4
+    first = rank * n  # this rank's shard of the global event index space
+    stream = torch.cuda.current_stream(dev)
+
+    # Inputs resident in HBM before the timed region.
+    v1, v2 = sd.muon_pairs(n, first=first, dtype=tdt, device=dev)
+    bv, bb = sd.boost_inputs(n, first=first, dtype=tdt, device=dev)
+    m = torch.empty(n, dtype=tdt, device=dev)
+    bout = torch.empty((n, 4), dtype=tdt, device=dev)
+    bins = gvx.new_bins(NB, dev)
+    bins_cm = gvx.new_bins(NB, dev)
+    torch.cuda.synchronize(dev)
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    kern_ms = {k: [] for k in KERNEL_ORDER}
+
+    def step(record: bool):
+        bins.zero_()
+        bins_cm.zero_()
+        if record:
+            ev[0].record(stream)
+        gvx.invariant_mass(v1, v2, out=m)
+        if record:
+            ev[1].record(stream)
+        gvx.boost(bv, bb, out=bout)
+        if record:
+            ev[2].record(stream)
+        gvx.mass_histogram(v1, v2, LO, HI, NB, bins=bins)
+        if record:
+            ev[3].record(stream)
+        gvx.mass_histogram(v1, v2, LO, HI, NB, bins=bins_cm, cm=True)
+        if record:
+            ev[4].record(stream)
+        if world > 1:
+            gvx.allreduce_bins(bins)
+            gvx.allreduce_bins(bins_cm)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(True)
+            ev[4].synchronize()
+            for i, k in enumerate(KERNEL_ORDER):
+                kern_ms[k].append(ev[i].elapsed_time(ev[i + 1]))
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+    elapsed_ms = t_start.elapsed_time(t_end)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = t.item()
+    ms_per_step = elapsed_ms / args.steps
+    value = n * world / (ms_per_step * 1e-3)
+
+    # per-kernel breakdown (CUDA events on the launch stream, averaged over the timed steps)
+    peak, peak_kind = peaks()
+    kernels = {}
+    for k in KERNEL_ORDER:
+        avg = sum(kern_ms[k]) / len(kern_ms[k])
+        bpe = BYTES[k](es)
+        gbs = n * bpe / (avg * 1e-3) / 1e9
+        kernels[k] = {"ms": avg, "events_per_s": n / (avg * 1e-3), "bytes_per_event": bpe,
+                      "achieved_GBs": gbs, "frac_of_peak": gbs / peak}
+    dom = max(KERNEL_ORDER, key=lambda k: kernels[k]["ms"])
+    roofline = {"bound": "hbm", "kernel": f"gvx_{dom}", "achieved": kernels[dom]["achieved_GBs"], "peak": peak,
+                "unit": "GB/s", "frac": kernels[dom]["frac_of_peak"], "traffic": ncu_traffic(dom, args.dtype),
+                "peak_source": peak_kind,
+                "bytes_per_launch": n * BYTES[dom](es)}
+
+    # e2e: the same step from pinned HOST buffers through the public API, copies timed
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, gvx, v1, v2, bv, bb, dev, stream, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_obj(args.cpu_sample, args.dtype)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (synth/: Philox4x32-10 seeded muon pairs + boost inputs, seed 12345)",
+            "config": config_obj(args, world),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 4 * args.steps, "clocks": clk.summary(), "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ncu_traffic(kernel: str, dtype: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    summary (profiles/ncu_traffic.json, written by tools/ncu_summary.py), else None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d[dtype][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def run_e2e(args, gvx, v1, v2, bv, bb, dev, stream, world):
+    """Whole step from pinned host memory: H2D of the inputs, the four kernels, D2H of
+    the masses, boosted vectors and bins — chunked over two streams so copies in both
+    directions overlap compute (public API: paper_2312_02756_b200.hostpipe)."""
+    import torch
+
+    from paper_2312_02756_b200 import hostpipe
+    import torch.distributed as dist
+    n = v1.shape[0]
+    h_v1 = torch.empty(v1.shape, dtype=v1.dtype, pin_memory=True)
+    h_v2 = torch.empty(v2.shape, dtype=v2.dtype, pin_memory=True)
+    h_bv = torch.empty(bv.shape, dtype=bv.dtype, pin_memory=True)
+    h_bb = torch.empty(bb.shape, dtype=bb.dtype, pin_memory=True)
+    for h, d in ((h_v1, v1), (h_v2, v2), (h_bv, bv), (h_bb, bb)):
+        h.copy_(d)
+    pipe = hostpipe.HostPipeline(n, v1.dtype, dev, nbins=NB, lo=LO, hi=HI)
+    for _ in range(max(1, args.warmup)):
+        res = pipe.step(h_v1, h_v2, h_bv, h_bb)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    steps = max(1, min(args.steps, 3))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        res = pipe.step(h_v1, h_v2, h_bv, h_bb)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    return {"value": n * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": pipe.h2d_bytes, "d2h_bytes_per_step": pipe.d2h_bytes,
+            "steps": steps, "path": "pinned host -> chunked H2D/compute/D2H over 2 streams (hostpipe)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * gvx.h — C ABI of the B200-native GenVectorX hot path (arXiv 2312.02756).
+ *
+ * Library: paper_2312_02756_b200/libgvx.so (hand-written sm_100a CUDA).
+ * No torch or CUDA types appear here: pointers are plain, sizes are int64,
+ * a stream is the opaque CUDA stream handle (cudaStream_t / CUstream are the
+ * same pointer; NULL = the legacy default stream).
+ *
+ * ---------------------------------------------------------------------------
+ * Common conventions (apply to every entry point below)
+ * ---------------------------------------------------------------------------
+ * Ownership. Every data pointer is caller-owned. Device entry points take
+ *   DEVICE pointers valid on the calling thread's current CUDA device; the
+ *   library allocates no device memory and keeps no mutable global state
+ *   (beyond a per-device SM-count cache filled once). Outputs are
+ *   caller-allocated, as in the paper's kernel signature
+ *   `(LVector *v1, LVector *v2, Scalar *m, size_t N)`.
+ * Asynchrony. Device entry points enqueue on `stream` and return without a
+ *   host synchronisation. Kernel faults surface at the caller's next sync.
+ * Errors. Arguments are validated synchronously and nothing is enqueued on
+ *   error: n < 0, a NULL component pointer with n > 0, stride < 1, a pointer
+ *   not aligned to sizeof(T), nbins < 1, non-finite lo/hi or lo >= hi
+ *   -> GVX_ERR_INVALID_ARGUMENT. n == 0 -> GVX_OK with nothing launched
+ *   (SPEC.md:280). A launch failure -> GVX_ERR_CUDA (details from
+ *   gvx_last_cuda_error_string()).
+ * Per-event domain problems never error (the paper drops exception
+ *   handling): NaN/Inf inputs propagate, a per-event |beta| >= 1
+ *   yields NaN x 4, NaN masses land in the overflow bin.
+ * Aliasing. A boost's output may be exactly its input (in place). Any other
+ *   overlap between an output and an input is undefined.
+ * Views. A 4-vector array is described by gvx_vec4_cview / gvx_vec4_view:
+ *   component k (0..3) of vector i is ((T*)c[k])[i * stride].
+ *     AoS [N][4]:        c[k] = base + k,     stride = 4
+ *     SoA 4 x [N]:       c[k] = array_k,      stride = 1
+ *     pairs [N][2][4]:   v1.c[k] = base + k, v2.c[k] = base + 4 + k, stride = 8
+ *   Component order is (pt, eta, phi, m) for GVX_PTETAPHIM and (px, py, pz, E)
+ *   for GVX_PXPYPZE (E last). Any view is accepted; AoS with
+ *   4*sizeof(T) alignment and SoA with 16-byte-aligned arrays take the
+ *   vectorised fast paths. Results are bitwise identical across layouts.
+ */
+#ifndef GVX_H
+#define GVX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GVX_ABI_VERSION 1
+
+typedef struct CUstream_st *gvx_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    GVX_OK = 0,
+    GVX_ERR_INVALID_ARGUMENT = 1,
+    GVX_ERR_DOMAIN = 2,
+    GVX_ERR_UNSUPPORTED = 3,
+    GVX_ERR_CUDA = 4
+} gvx_status;
+
+typedef enum { GVX_F32 = 0, GVX_F64 = 1 } gvx_dtype;
+
+/* 4D coordinate systems ("any 4-dimensional
+ * coordinate system"). Mass and histogram accept both; boost takes PXPYPZE. */
+typedef enum { GVX_PTETAPHIM = 0, GVX_PXPYPZE = 1 } gvx_coords;
+
+typedef struct { const void *c[4]; int64_t stride; } gvx_vec4_cview;
+typedef struct { void *c[4]; int64_t stride; } gvx_vec4_view;
+typedef struct { const void *c[3]; int64_t stride; } gvx_vec3_cview;
+
+/* Flags of gvx_mass_histogram. */
+#define GVX_HIST_BOOST_TO_CM 0x1u
+
+/*
+ * gvx_invariant_mass — InvariantMasses (Fig. 1):
+ *   m_out[i] = (v1[i] + v2[i]).mass()
+ * The sum is component-wise in PxPyPzE; PtEtaPhiM input
+ * is converted with px = pt cos(phi), py = pt sin(phi), pz = pt sinh(eta),
+ * E = sqrt(max(0, m|m| + pt^2 + pz^2)) (clamp = DESIGN.md R2).
+ * mass() = sqrt(M^2) if M^2 >= 0 else -sqrt(-M^2), M^2 = E^2 - |p|^2
+ * (SPEC.md:101-103, :138).
+ *   dtype   GVX_F32 / GVX_F64: element type of v1, v2 and m_out (arithmetic
+ *           is closed over it).
+ *   v1, v2  n input vectors each (device).
+ *   m_out   n masses, contiguous (device), must not overlap the inputs.
+ * Accuracy: |M_gpu|M_gpu| - M_exact^2| <= tau * E_lab^2 with tau = 1e-12
+ * (f64) / 1e-5 (f32), E_lab = E1 + E2 (north_star; R5).
+ */
+gvx_status gvx_invariant_mass(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview *v1,
+                              const gvx_vec4_cview *v2, void *m_out, int64_t n,
+                              gvx_stream_t stream);
+
+/*
+ * gvx_boost — ApplyBoost with a per-event velocity ("a
+ * 4-dimensional Lorentz transformation represented internally by a 4x4
+ * orthosymplectic matrix"; matrix SPEC.md:188):
+ *   gamma = 1/sqrt(1 - b^2), L_ij = d_ij + gamma^2/(1+gamma) b_i b_j,
+ *   L_i4 = L_4i = gamma b_i, L_44 = gamma;  out[i] = L(beta[i]) * v[i]
+ * (active boost, metric diag(-1,-1,-1,+1); R6, R7).
+ *   v     n PxPyPzE vectors (device);  beta  n velocities (bx, by, bz) (device)
+ *   out   n PxPyPzE vectors (device); may equal v exactly (in place).
+ * |beta[i]| >= 1 or NaN -> out[i] = NaN x 4. Accuracy: component-wise
+ * |delta| <= tau * S, S = gamma (E + |beta||p|) (R5).
+ */
+gvx_status gvx_boost(gvx_dtype dtype, const gvx_vec4_cview *v, const gvx_vec3_cview *beta,
+                     const gvx_vec4_view *out, int64_t n, gvx_stream_t stream);
+
+/*
+ * gvx_boost_uniform — the paper's single-matrix ApplyBoost:
+ * one beta = (bx, by, bz) for all n vectors (rounded to dtype first).
+ * |beta| >= 1 or non-finite -> GVX_ERR_DOMAIN, nothing enqueued.
+ */
+gvx_status gvx_boost_uniform(gvx_dtype dtype, const gvx_vec4_cview *v, double bx, double by,
+                             double bz, const gvx_vec4_view *out, int64_t n,
+                             gvx_stream_t stream);
+
+/*
+ * gvx_mass_histogram — fused InvariantMass + histogram (north_star;
+ * BASELINE.json configs[3], configs[4]). For each pair the signed mass M (as
+ * gvx_invariant_mass; with flags & GVX_HIST_BOOST_TO_CM, the mass after
+ * boosting both vectors by beta_cm = -(p1+p2)/(E1+E2), R11; E <= 0
+ * or beta_cm^2 >= 1 -> NaN) is promoted to double and binned ROOT-style
+ * (R12):  x < lo -> 0;  !(x < hi) (NaN included) -> nbins+1;
+ *                   else 1 + (int)((nbins * (x - lo)) / (hi - lo)).
+ *   bins         nbins+2 uint64 counters (device), ACCUMULATED (caller zeroes);
+ *                this is the per-shard stage of the multi-GPU reduction.
+ *   m_out        NULL or n masses of dtype (device).
+ *   boosted_out  NULL or, with GVX_HIST_BOOST_TO_CM, 2n boosted PxPyPzE
+ *                vectors: pair i -> vectors 2i and 2i+1 of the view.
+ */
+gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview *v1,
+                              const gvx_vec4_cview *v2, int64_t n, double lo, double hi,
+                              int32_t nbins, unsigned long long *bins, uint32_t flags,
+                              void *m_out, const gvx_vec4_view *boosted_out,
+                              gvx_stream_t stream);
+
+/* Human-readable name of a status code (static storage). */
+const char *gvx_status_string(gvx_status status);
+/* The CUDA error string behind the last GVX_ERR_CUDA on this thread. */
+const char *gvx_last_cuda_error_string(void);
+/* GVX_ABI_VERSION of the loaded library. */
+int gvx_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GVX_H */

@@ -1,0 +1,308 @@
+"""B200-native GenVectorX hot path (arXiv 2312.02756): Python binding.
+
+Thin marshalling over the C ABI of ``include/gvx.h`` (``libgvx.so``, hand-
+written sm_100a CUDA). Torch supplies device memory and the current stream
+only; every step of the path runs in the library's kernels. There is no CPU
+fallback: importing this package on a machine where ``libgvx.so`` is missing
+raises, and calling an op with CPU tensors raises.
+
+Names follow the paper ("InvariantMasses", "ApplyBoost"):
+
+* :func:`invariant_mass` — ``m[i] = (v1[i] + v2[i]).mass()`` (Fig. 1)
+* :func:`boost` / :func:`boost_uniform` — Lorentz boost by per-event / one β
+* :func:`mass_histogram` — fused mass (+ optional CM boost) histogram
+* :func:`sharded_mass_histogram` — per-rank histogram + NCCL bin all-reduce
+
+Vector arguments are CUDA tensors ``[N, 4]`` (AoS, any row stride — e.g. the
+``[:, 0, :]`` view of interleaved ``[N, 2, 4]`` pairs) or a 4-sequence of
+``[N]`` tensors sharing one stride (SoA). Components are (pt, eta, phi, m)
+for ``coords="ptetaphim"`` and (px, py, pz, E) for ``coords="pxpypze"``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence, Union
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgvx.so")
+
+GVX_OK = 0
+GVX_ERR_INVALID_ARGUMENT = 1
+GVX_ERR_DOMAIN = 2
+GVX_ERR_UNSUPPORTED = 3
+GVX_ERR_CUDA = 4
+GVX_F32 = 0
+GVX_F64 = 1
+GVX_PTETAPHIM = 0
+GVX_PXPYPZE = 1
+GVX_HIST_BOOST_TO_CM = 0x1
+ABI_VERSION = 1
+
+# The default histogram of the north star: 1000 bins over the dimuon range
+# (reading R13).
+DEFAULT_LO = 0.25
+DEFAULT_HI = 300.0
+DEFAULT_NBINS = 1000
+
+
+class Vec4CView(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_void_p * 4), ("stride", ctypes.c_int64)]
+
+
+class Vec4View(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_void_p * 4), ("stride", ctypes.c_int64)]
+
+
+class Vec3CView(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_void_p * 3), ("stride", ctypes.c_int64)]
+
+
+class GvxError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+class DomainError(GvxError, ValueError):
+    pass
+
+
+def _load_lib():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    I64 = ctypes.c_int64
+    st = ctypes.c_int
+    lib.gvx_invariant_mass.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), P, I64, P]
+    lib.gvx_invariant_mass.restype = st
+    lib.gvx_boost.argtypes = [st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec3CView), ctypes.POINTER(Vec4View),
+                              I64, P]
+    lib.gvx_boost.restype = st
+    lib.gvx_boost_uniform.argtypes = [st, ctypes.POINTER(Vec4CView), ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, ctypes.POINTER(Vec4View), I64, P]
+    lib.gvx_boost_uniform.restype = st
+    lib.gvx_mass_histogram.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, ctypes.c_uint32, P,
+                                       ctypes.POINTER(Vec4View), P]
+    lib.gvx_mass_histogram.restype = st
+    lib.gvx_status_string.argtypes = [st]
+    lib.gvx_status_string.restype = ctypes.c_char_p
+    lib.gvx_last_cuda_error_string.argtypes = []
+    lib.gvx_last_cuda_error_string.restype = ctypes.c_char_p
+    lib.gvx_abi_version.restype = ctypes.c_int
+    if lib.gvx_abi_version() != ABI_VERSION:
+        raise ImportError(f"libgvx ABI {lib.gvx_abi_version()} != binding ABI {ABI_VERSION}")
+    return lib
+
+
+lib = _load_lib()
+
+VecArg = Union[torch.Tensor, Sequence[torch.Tensor]]
+
+
+def _check(status: int, what: str) -> None:
+    if status == GVX_OK:
+        return
+    name = lib.gvx_status_string(status).decode()
+    if status == GVX_ERR_CUDA:
+        raise GvxError(status, f"{what}: {name}: {lib.gvx_last_cuda_error_string().decode()}")
+    if status == GVX_ERR_DOMAIN:
+        raise DomainError(status, f"{what}: {name}")
+    raise GvxError(status, f"{what}: {name}")
+
+
+def _dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float64:
+        return GVX_F64
+    if dt == torch.float32:
+        return GVX_F32
+    raise TypeError(f"gvx supports float32 and float64, got {dt}")
+
+
+def _coords_code(coords: str) -> int:
+    try:
+        return {"ptetaphim": GVX_PTETAPHIM, "pxpypze": GVX_PXPYPZE}[coords]
+    except KeyError:
+        raise ValueError(f"coords must be 'ptetaphim' or 'pxpypze', got {coords!r}") from None
+
+
+def _require_cuda(t: torch.Tensor, name: str) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (gvx has no CPU fallback)")
+
+
+def _view(x: VecArg, ncomp: int, name: str, writable: bool = False):
+    """-> (ctypes view struct, n, dtype, device, keepalive)."""
+    if isinstance(x, torch.Tensor):
+        _require_cuda(x, name)
+        if x.dim() != 2 or x.shape[1] != ncomp:
+            raise ValueError(f"{name} must be [N, {ncomp}] or a {ncomp}-sequence of [N] tensors, got {tuple(x.shape)}")
+        es = x.element_size()
+        base = x.data_ptr()
+        s0, s1 = x.stride()
+        n = x.shape[0]
+        ptrs = [base + k * s1 * es for k in range(ncomp)]
+        stride = s0 if n > 1 else max(s0, 1)
+        dtype, dev = x.dtype, x.device
+        keep = (x,)
+    else:
+        comps = list(x)
+        if len(comps) != ncomp:
+            raise ValueError(f"{name} must have {ncomp} components, got {len(comps)}")
+        for i, c in enumerate(comps):
+            _require_cuda(c, f"{name}[{i}]")
+            if c.dim() != 1:
+                raise ValueError(f"{name}[{i}] must be 1-D")
+        n = comps[0].shape[0]
+        dtype, dev = comps[0].dtype, comps[0].device
+        if any(c.shape[0] != n or c.dtype != dtype or c.device != dev for c in comps):
+            raise ValueError(f"{name}: components differ in length, dtype or device")
+        strides = {c.stride(0) for c in comps} if n > 1 else {1}
+        if len(strides) != 1:
+            raise ValueError(f"{name}: components must share one stride")
+        stride = strides.pop()
+        ptrs = [c.data_ptr() for c in comps]
+        keep = tuple(comps)
+    if ncomp == 4:
+        v = (Vec4View if writable else Vec4CView)()
+    else:
+        v = Vec3CView()
+    for k in range(ncomp):
+        v.c[k] = ptrs[k]
+    v.stride = max(int(stride), 1)
+    return v, n, dtype, dev, keep
+
+
+def _stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def invariant_mass(v1: VecArg, v2: VecArg, out: Optional[torch.Tensor] = None,
+                   coords: str = "ptetaphim") -> torch.Tensor:
+    """InvariantMasses: ``out[i] = (v1[i] + v2[i]).mass()``, signed (ROOT convention)."""
+    a, n, dt, dev, k1 = _view(v1, 4, "v1")
+    b, n2, dt2, dev2, k2 = _view(v2, 4, "v2")
+    if n != n2:
+        raise ValueError(f"length mismatch: v1 has {n} vectors, v2 has {n2}")
+    if dt != dt2 or dev != dev2:
+        raise ValueError("v1 and v2 must share dtype and device")
+    if out is None:
+        out = torch.empty(n, dtype=dt, device=dev)
+    else:
+        _require_cuda(out, "out")
+        if out.shape != (n,) or out.dtype != dt or not out.is_contiguous() or out.device != dev:
+            raise ValueError("out must be a contiguous [N] tensor of the inputs' dtype and device")
+    with torch.cuda.device(dev):
+        _check(lib.gvx_invariant_mass(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b),
+                                      out.data_ptr() if n else None, n, _stream(dev)), "gvx_invariant_mass")
+    return out
+
+
+def _boost_out(v_t, n, dt, dev, out):
+    if out is None:
+        out = torch.empty((n, 4), dtype=dt, device=dev)
+    o, no, dto, devo, ko = _view(out, 4, "out", writable=True)
+    if no != n or dto != dt or devo != dev:
+        raise ValueError("out must match v in length, dtype and device")
+    return out, o
+
+
+def boost(v: VecArg, beta: VecArg, out: Optional[VecArg] = None) -> VecArg:
+    """ApplyBoost with per-event β: ``out[i] = Λ(β[i])·v[i]``.
+
+    ``v`` PxPyPzE; ``out`` may be ``v`` itself (in place). |β[i]| ≥ 1 → NaN×4.
+    """
+    a, n, dt, dev, k1 = _view(v, 4, "v")
+    b, nb, dtb, devb, k2 = _view(beta, 3, "beta")
+    if nb != n:
+        raise ValueError(f"length mismatch: v has {n} vectors, beta has {nb}")
+    if dtb != dt or devb != dev:
+        raise ValueError("v and beta must share dtype and device")
+    out, o = _boost_out(v, n, dt, dev, out)
+    with torch.cuda.device(dev):
+        _check(lib.gvx_boost(_dtype_code(dt), ctypes.byref(a), ctypes.byref(b), ctypes.byref(o), n, _stream(dev)),
+               "gvx_boost")
+    return out
+
+
+def boost_uniform(v: VecArg, beta: Sequence[float], out: Optional[VecArg] = None) -> VecArg:
+    """The paper's single-matrix ApplyBoost; |β| ≥ 1 raises :class:`DomainError`."""
+    a, n, dt, dev, k1 = _view(v, 4, "v")
+    bx, by, bz = (float(x) for x in beta)
+    out, o = _boost_out(v, n, dt, dev, out)
+    with torch.cuda.device(dev):
+        _check(lib.gvx_boost_uniform(_dtype_code(dt), ctypes.byref(a), bx, by, bz, ctypes.byref(o), n,
+                                     _stream(dev)), "gvx_boost_uniform")
+    return out
+
+
+def new_bins(nbins: int = DEFAULT_NBINS, device=None) -> torch.Tensor:
+    """Zeroed counters: [nbins + 2] int64 (0 = underflow, nbins + 1 = overflow)."""
+    return torch.zeros(nbins + 2, dtype=torch.int64, device=device or torch.device("cuda"))
+
+
+def mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = DEFAULT_HI,
+                   nbins: int = DEFAULT_NBINS, bins: Optional[torch.Tensor] = None, cm: bool = False,
+                   m_out: Optional[torch.Tensor] = None, boosted_out: Optional[VecArg] = None,
+                   coords: str = "ptetaphim") -> torch.Tensor:
+    """Fused mass histogram (north star). Accumulates into ``bins`` ([nbins+2] int64, zeroed by the caller
+    or allocated here) and returns it. ``cm=True`` boosts each pair to its CM frame first.
+    ``boosted_out`` ([2N, 4], CM only) receives the boosted pair (vectors 2i, 2i+1)."""
+    a, n, dt, dev, k1 = _view(v1, 4, "v1")
+    b, n2, dt2, dev2, k2 = _view(v2, 4, "v2")
+    if n != n2:
+        raise ValueError(f"length mismatch: v1 has {n} vectors, v2 has {n2}")
+    if dt != dt2 or dev != dev2:
+        raise ValueError("v1 and v2 must share dtype and device")
+    if bins is None:
+        bins = new_bins(nbins, dev)
+    _require_cuda(bins, "bins")
+    if bins.shape != (nbins + 2,) or bins.dtype != torch.int64 or not bins.is_contiguous():
+        raise ValueError(f"bins must be a contiguous int64 tensor of shape [{nbins + 2}]")
+    mptr = None
+    if m_out is not None:
+        _require_cuda(m_out, "m_out")
+        if m_out.shape != (n,) or m_out.dtype != dt or not m_out.is_contiguous():
+            raise ValueError("m_out must be a contiguous [N] tensor of the inputs' dtype")
+        mptr = m_out.data_ptr()
+    bo_ref = None
+    if boosted_out is not None:
+        if not cm:
+            raise ValueError("boosted_out requires cm=True")
+        bo, nbo, dtbo, devbo, kbo = _view(boosted_out, 4, "boosted_out", writable=True)
+        if nbo != 2 * n or dtbo != dt:
+            raise ValueError("boosted_out must hold 2N vectors of the inputs' dtype")
+        bo_ref = ctypes.byref(bo)
+    flags = GVX_HIST_BOOST_TO_CM if cm else 0
+    with torch.cuda.device(dev):
+        _check(lib.gvx_mass_histogram(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b), n,
+                                      float(lo), float(hi), int(nbins), bins.data_ptr(), flags, mptr, bo_ref,
+                                      _stream(dev)), "gvx_mass_histogram")
+    return bins
+
+
+def sharded_mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = DEFAULT_HI,
+                           nbins: int = DEFAULT_NBINS, cm: bool = False, group=None,
+                           coords: str = "ptetaphim", bins: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Per-rank fused histogram of this rank's event shard, then ONE all-reduce(SUM) of the
+    nbins+2 counters over the process group (NCCL over NVLink on B200s; gloo on CPU tests).
+    Returns the global histogram on every rank."""
+    bins = mass_histogram(v1, v2, lo, hi, nbins, bins=bins, cm=cm, coords=coords)
+    return allreduce_bins(bins, group)
+
+
+def allreduce_bins(bins: torch.Tensor, group=None) -> torch.Tensor:
+    """The path's only cross-rank exchange: all-reduce(SUM) of the int64
+    bin counters, in place. No-op without an initialised multi-rank process group."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(bins, op=dist.ReduceOp.SUM, group=group)
+    return bins

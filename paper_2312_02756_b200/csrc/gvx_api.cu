@@ -1,0 +1,292 @@
+// gvx_api.cu — the C ABI (include/gvx.h): validation, layout detection,
+// kernel selection and persistent-grid launch. No allocation, no host sync.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+
+#include "../../include/gvx.h"
+#include "gvx_kernels.cuh"
+
+using namespace gvx;
+
+namespace {
+
+thread_local std::string g_last_cuda_error = "no error";
+
+gvx_status cuda_fail(cudaError_t e) {
+  g_last_cuda_error = cudaGetErrorString(e);
+  return GVX_ERR_CUDA;
+}
+
+// Per-device SM count, filled once (the only library state).
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sm_count[kMaxDevices];
+
+int sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
+  int v = g_sm_count[dev].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  g_sm_count[dev].store(sms, std::memory_order_relaxed);
+  return sms;
+}
+
+// Persistent grid: enough CTAs to fill every SM at the kernel's occupancy,
+// never more than the work needs.
+template <typename K>
+int grid_for(K kernel, int block, size_t smem, int64_t work_items_per_block_pass, int64_t items) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  int64_t full = (int64_t)sm_count() * per_sm;
+  int64_t need = (items + work_items_per_block_pass - 1) / work_items_per_block_pass;
+  if (need < 1) need = 1;
+  return (int)(need < full ? need : full);
+}
+
+inline bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+size_t dsize(gvx_dtype d) { return d == GVX_F64 ? 8 : 4; }
+
+bool valid_dtype(gvx_dtype d) { return d == GVX_F32 || d == GVX_F64; }
+bool valid_coords(gvx_coords c) { return c == GVX_PTETAPHIM || c == GVX_PXPYPZE; }
+
+template <int NC, typename V>
+bool view_ok(const V* v, size_t es) {
+  if (!v || v->stride < 1) return false;
+  for (int k = 0; k < NC; ++k)
+    if (!v->c[k] || !aligned(v->c[k], es)) return false;
+  return true;
+}
+
+// Layout classification of an input 4-vector view (see gvx_kernels.cuh).
+template <typename V>
+int classify(const V* v, size_t es) {
+  const char* b = (const char*)v->c[0];
+  bool contiguous_aos = v->stride == 4;
+  for (int k = 1; k < 4; ++k) contiguous_aos = contiguous_aos && (const char*)v->c[k] == b + k * es;
+  if (contiguous_aos && aligned(b, 32)) return L_AOS;  // 256-bit loads need 32-byte alignment
+  if (v->stride == 1) {
+    bool ok = true;
+    for (int k = 0; k < 4; ++k) ok = ok && aligned(v->c[k], 32);
+    if (ok) return L_SOA;
+  }
+  return L_GEN;
+}
+
+template <typename T>
+View4<T> mk4(const gvx_vec4_cview* v) {
+  View4<T> r;
+  for (int k = 0; k < 4; ++k) r.c[k] = (const T*)v->c[k];
+  r.s = v->stride;
+  return r;
+}
+template <typename T>
+View4o<T> mk4o(const gvx_vec4_view* v) {
+  View4o<T> r;
+  for (int k = 0; k < 4; ++k) r.c[k] = v ? (T*)v->c[k] : nullptr;
+  r.s = v ? v->stride : 1;
+  return r;
+}
+template <typename T>
+View3<T> mk3(const gvx_vec3_cview* v) {
+  View3<T> r;
+  for (int k = 0; k < 3; ++k) r.c[k] = v ? (const T*)v->c[k] : nullptr;
+  r.s = v ? v->stride : 1;
+  return r;
+}
+
+constexpr int kBlock = 256;
+
+// ---------------------------------------------------------------- mass ------
+template <typename T, int C, int L>
+gvx_status launch_mass(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, void* m, int64_t n, cudaStream_t s) {
+  constexpr int U = (L == L_AOS && sizeof(T) == 8) ? 2 : 1;
+  constexpr int G = Group<T, L>::G;
+  auto k = k_invariant_mass<T, C, L, U>;
+  int grid = grid_for(k, kBlock, 0, (int64_t)kBlock * U * G, n);
+  k<<<grid, kBlock, 0, s>>>(mk4<T>(v1), mk4<T>(v2), (T*)m, n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+template <typename T, int C>
+gvx_status dispatch_mass(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, void* m, int64_t n, cudaStream_t s) {
+  int l1 = classify(v1, sizeof(T)), l2 = classify(v2, sizeof(T));
+  int L = (l1 == l2) ? l1 : L_GEN;
+  if (L == L_AOS && !aligned(m, Group<T, L_AOS>::G * sizeof(T))) L = L_GEN;  // vector stores
+  if (L == L_SOA && !aligned(m, Group<T, L_SOA>::G * sizeof(T))) L = L_GEN;
+  if (L == L_AOS) return launch_mass<T, C, L_AOS>(v1, v2, m, n, s);
+  if (L == L_SOA) return launch_mass<T, C, L_SOA>(v1, v2, m, n, s);
+  return launch_mass<T, C, L_GEN>(v1, v2, m, n, s);
+}
+
+// ---------------------------------------------------------------- boost -----
+template <typename T, bool UNI>
+gvx_status launch_boost(const gvx_vec4_cview* v, const gvx_vec3_cview* beta, const gvx_vec4_view* out, int64_t n,
+                        T bx, T by, T bz, cudaStream_t s) {
+  const char* vb = (const char*)v->c[0];
+  const char* ob = (const char*)out->c[0];
+  bool aos = v->stride == 4 && out->stride == 4 && aligned(vb, 4 * sizeof(T)) && aligned(ob, 4 * sizeof(T));
+  for (int k = 1; k < 4; ++k)
+    aos = aos && (const char*)v->c[k] == vb + k * sizeof(T) && (const char*)out->c[k] == ob + k * sizeof(T);
+  if (aos) {
+    auto k = k_boost<T, true, UNI>;
+    int grid = grid_for(k, kBlock, 0, kBlock, n);
+    k<<<grid, kBlock, 0, s>>>(mk4<T>(v), mk3<T>(beta), mk4o<T>(out), n, bx, by, bz);
+  } else {
+    auto k = k_boost<T, false, UNI>;
+    int grid = grid_for(k, kBlock, 0, kBlock, n);
+    k<<<grid, kBlock, 0, s>>>(mk4<T>(v), mk3<T>(beta), mk4o<T>(out), n, bx, by, bz);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+// Output may equal the input exactly (in place); any other overlap is UB.
+bool out_view_ok(const gvx_vec4_view* out, size_t es) { return view_ok<4>(out, es); }
+
+// ---------------------------------------------------------------- hist ------
+constexpr size_t kMaxSmemBins = 48 * 1024;  // uint32 bins in shared memory (192 KB)
+
+template <typename T, int C, int L, bool CM>
+gvx_status launch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, const HistParams& hp,
+                       unsigned long long* bins, void* m_out, const gvx_vec4_view* bo, cudaStream_t s) {
+  constexpr int G = Group<T, L>::G;
+  size_t nb2 = (size_t)hp.nbins + 2;
+  bool smem = nb2 <= kMaxSmemBins;
+  View4o<T> bov = mk4o<T>(bo);
+  cudaError_t e;
+  if (smem) {
+    auto k = k_mass_histogram<T, C, L, CM, true>;
+    size_t sm = nb2 * sizeof(unsigned int);
+    if (sm > 48 * 1024 && (e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
+      return cuda_fail(e);
+    int grid = grid_for(k, kBlock, sm, (int64_t)kBlock * G, n);
+    // Per-CTA uint32 counters: one launch covers at most grid * 2^31 events.
+    const int64_t chunk = (int64_t)grid << 31;
+    for (int64_t off = 0; off < n; off += chunk) {
+      int64_t cn = n - off < chunk ? n - off : chunk;
+      View4<T> a = mk4<T>(v1), b = mk4<T>(v2);
+      View4o<T> bo2 = bov;
+      for (int c = 0; c < 4; ++c) {
+        a.c[c] += off * a.s;
+        b.c[c] += off * b.s;
+        if (bo) bo2.c[c] += 2 * off * bo2.s;
+      }
+      T* mo = m_out ? (T*)m_out + off : nullptr;
+      k<<<grid, kBlock, sm, s>>>(a, b, cn, hp, bins, mo, bo2, bo != nullptr);
+    }
+  } else {
+    auto k = k_mass_histogram<T, C, L, CM, false>;
+    int grid = grid_for(k, kBlock, 0, (int64_t)kBlock * G, n);
+    k<<<grid, kBlock, 0, s>>>(mk4<T>(v1), mk4<T>(v2), n, hp, bins, (T*)m_out, bov, bo != nullptr);
+  }
+  e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+template <typename T, int C, bool CM>
+gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, const HistParams& hp,
+                         unsigned long long* bins, void* m_out, const gvx_vec4_view* bo, cudaStream_t s) {
+  int l1 = classify(v1, sizeof(T)), l2 = classify(v2, sizeof(T));
+  int L = (l1 == l2) ? l1 : L_GEN;
+  if (m_out && L == L_AOS && !aligned(m_out, Group<T, L_AOS>::G * sizeof(T))) L = L_GEN;
+  if (m_out && L == L_SOA && !aligned(m_out, Group<T, L_SOA>::G * sizeof(T))) L = L_GEN;
+  if (L == L_AOS) return launch_hist<T, C, L_AOS, CM>(v1, v2, n, hp, bins, m_out, bo, s);
+  if (L == L_SOA) return launch_hist<T, C, L_SOA, CM>(v1, v2, n, hp, bins, m_out, bo, s);
+  return launch_hist<T, C, L_GEN, CM>(v1, v2, n, hp, bins, m_out, bo, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gvx_abi_version(void) { return GVX_ABI_VERSION; }
+
+const char* gvx_status_string(gvx_status st) {
+  switch (st) {
+    case GVX_OK: return "GVX_OK";
+    case GVX_ERR_INVALID_ARGUMENT: return "GVX_ERR_INVALID_ARGUMENT";
+    case GVX_ERR_DOMAIN: return "GVX_ERR_DOMAIN";
+    case GVX_ERR_UNSUPPORTED: return "GVX_ERR_UNSUPPORTED";
+    case GVX_ERR_CUDA: return "GVX_ERR_CUDA";
+  }
+  return "GVX_ERR_UNKNOWN";
+}
+
+const char* gvx_last_cuda_error_string(void) { return g_last_cuda_error.c_str(); }
+
+gvx_status gvx_invariant_mass(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1, const gvx_vec4_cview* v2,
+                              void* m_out, int64_t n, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || !valid_coords(coords) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GVX_OK;
+  size_t es = dsize(dtype);
+  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !m_out || !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GVX_F64)
+    return coords == GVX_PTETAPHIM ? dispatch_mass<double, C_PTETAPHIM>(v1, v2, m_out, n, s)
+                                   : dispatch_mass<double, C_PXPYPZE>(v1, v2, m_out, n, s);
+  return coords == GVX_PTETAPHIM ? dispatch_mass<float, C_PTETAPHIM>(v1, v2, m_out, n, s)
+                                 : dispatch_mass<float, C_PXPYPZE>(v1, v2, m_out, n, s);
+}
+
+gvx_status gvx_boost(gvx_dtype dtype, const gvx_vec4_cview* v, const gvx_vec3_cview* beta, const gvx_vec4_view* out,
+                     int64_t n, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GVX_OK;
+  size_t es = dsize(dtype);
+  if (!view_ok<4>(v, es) || !view_ok<3>(beta, es) || !out_view_ok(out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GVX_F64) return launch_boost<double, false>(v, beta, out, n, 0, 0, 0, s);
+  return launch_boost<float, false>(v, beta, out, n, 0, 0, 0, s);
+}
+
+gvx_status gvx_boost_uniform(gvx_dtype dtype, const gvx_vec4_cview* v, double bx, double by, double bz,
+                             const gvx_vec4_view* out, int64_t n, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (!isfinite(bx) || !isfinite(by) || !isfinite(bz)) return GVX_ERR_DOMAIN;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GVX_F64) {
+    if (!(bx * bx + by * by + bz * bz < 1.0)) return GVX_ERR_DOMAIN;
+  } else {
+    float fx = (float)bx, fy = (float)by, fz = (float)bz;
+    if (!(fx * fx + fy * fy + fz * fz < 1.0f)) return GVX_ERR_DOMAIN;
+  }
+  if (n == 0) return GVX_OK;
+  size_t es = dsize(dtype);
+  if (!view_ok<4>(v, es) || !out_view_ok(out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  if (dtype == GVX_F64) return launch_boost<double, true>(v, nullptr, out, n, bx, by, bz, s);
+  return launch_boost<float, true>(v, nullptr, out, n, (float)bx, (float)by, (float)bz, s);
+}
+
+gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1, const gvx_vec4_cview* v2,
+                              int64_t n, double lo, double hi, int32_t nbins, unsigned long long* bins, uint32_t flags,
+                              void* m_out, const gvx_vec4_view* boosted_out, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || !valid_coords(coords) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
+  if ((flags & ~GVX_HIST_BOOST_TO_CM) != 0u) return GVX_ERR_INVALID_ARGUMENT;
+  bool cm = (flags & GVX_HIST_BOOST_TO_CM) != 0u;
+  if (boosted_out && !cm) return GVX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GVX_OK;
+  size_t es = dsize(dtype);
+  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !bins || !aligned(bins, 8)) return GVX_ERR_INVALID_ARGUMENT;
+  if (m_out && !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  if (boosted_out && !out_view_ok(boosted_out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  HistParams hp{lo, hi, hi - lo, nbins};
+  cudaStream_t s = (cudaStream_t)stream;
+#define GVX_HIST_DISPATCH(T, C)                                                                                  \
+  (cm ? dispatch_hist<T, C, true>(v1, v2, n, hp, bins, m_out, boosted_out, s)                       \
+      : dispatch_hist<T, C, false>(v1, v2, n, hp, bins, m_out, boosted_out, s))
+  if (dtype == GVX_F64) return coords == GVX_PTETAPHIM ? GVX_HIST_DISPATCH(double, C_PTETAPHIM) : GVX_HIST_DISPATCH(double, C_PXPYPZE);
+  return coords == GVX_PTETAPHIM ? GVX_HIST_DISPATCH(float, C_PTETAPHIM) : GVX_HIST_DISPATCH(float, C_PXPYPZE);
+#undef GVX_HIST_DISPATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,276 @@
+// gvx_kernels.cuh — sm_100a kernels of the GenVectorX hot path.
+//
+// Structure: persistent grid-stride kernels, one grid of
+// (148 SMs x resident CTAs), each thread moving U "groups" per iteration with
+// warp-contiguous 256-bit loads (LDG.E.ENL2.256) so that every load
+// instruction of a warp covers 1 KiB of consecutive HBM:
+//   AoS f64: group = 1 event  (v[i] is one 32-byte vector)
+//   AoS f32: group = 2 events (two 16-byte vectors per 256-bit load)
+//   SoA f64: group = 4 events, SoA f32: group = 8 events (per component)
+//   generic strided view: group = 1 event, scalar loads.
+// Events n % G at the end (and misaligned views) use scalar loads.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gvx_math.cuh"
+
+namespace gvx {
+
+enum Layout { L_AOS = 0, L_SOA = 1, L_GEN = 2 };
+enum Coords { C_PTETAPHIM = 0, C_PXPYPZE = 1 };
+
+template <typename T> struct View4 { const T* c[4]; int64_t s; };
+template <typename T> struct View4o { T* c[4]; int64_t s; };
+template <typename T> struct View3 { const T* c[3]; int64_t s; };
+
+template <typename T, int L> struct Group {
+  static constexpr int G = (L == L_AOS) ? (32 / (4 * (int)sizeof(T))) : (L == L_SOA) ? (32 / (int)sizeof(T)) : 1;
+};
+
+// ---- 256-bit streaming loads / stores (inline PTX; sm_100 v4.f64 / v8.f32) --
+__device__ __forceinline__ void ld256(const double* p, double (&r)[4]) {
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld256(const float* p, float (&r)[8]) {
+  asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void st256(double* p, const double (&r)[4]) {
+  asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r[0]), "d"(r[1]),
+               "d"(r[2]), "d"(r[3]) : "memory");
+}
+__device__ __forceinline__ void st256(float* p, const float (&r)[8]) {
+  asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r[0]),
+               "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]) : "memory");
+}
+
+// Load group g of a 4-vector view: x[k][j] = component k of event g*G + j.
+template <typename T, int L>
+__device__ __forceinline__ void load_group(const View4<T>& v, int64_t g, T (&x)[4][Group<T, L>::G]) {
+  constexpr int G = Group<T, L>::G;
+  if constexpr (L == L_AOS) {
+    constexpr int W = 32 / sizeof(T);  // scalars per 256-bit load = 4*G
+    T r[W];
+    ld256(v.c[0] + g * W, r);
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[k][j] = r[4 * j + k];
+  } else if constexpr (L == L_SOA) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      T r[G];
+      ld256(v.c[k] + g * G, r);
+#pragma unroll
+      for (int j = 0; j < G; ++j) x[k][j] = r[j];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k][0] = __ldg(v.c[k] + g * v.s);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load_event(const View4<T>& v, int64_t i, T (&x)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) x[k] = __ldg(v.c[k] + i * v.s);
+}
+
+// Store G contiguous results.
+template <typename T, int G>
+__device__ __forceinline__ void store_group(T* __restrict__ out, int64_t g, const T (&m)[G]) {
+  if constexpr (G * sizeof(T) == 32) {
+    st256(out + g * G, m);
+  } else if constexpr (G == 2 && sizeof(T) == 4) {
+    *reinterpret_cast<float2*>(out + g * 2) = make_float2(m[0], m[1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < G; ++j) out[g * G + j] = m[j];
+  }
+}
+
+template <typename T, int COORDS>
+__device__ __forceinline__ T event_mass(const T (&a)[4], const T (&b)[4]) {
+  if constexpr (COORDS == C_PTETAPHIM) {
+    return pair_mass_ptetaphim(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3]);
+  } else {
+    V4<T> x{a[0], a[1], a[2], a[3]}, y{b[0], b[1], b[2], b[3]};
+    return mass_of_sum(x, y);
+  }
+}
+
+template <typename T, int COORDS>
+__device__ __forceinline__ V4<T> to_cartesian(const T (&a)[4]) {
+  if constexpr (COORDS == C_PTETAPHIM) return ptetaphim_to_cartesian(a[0], a[1], a[2], a[3]);
+  else return V4<T>{a[0], a[1], a[2], a[3]};
+}
+
+// ============================================================================
+// K1: invariant mass
+// ============================================================================
+template <typename T, int COORDS, int L, int U>
+__global__ void __launch_bounds__(256) k_invariant_mass(View4<T> v1, View4<T> v2, T* __restrict__ m, int64_t n) {
+  constexpr int G = Group<T, L>::G;
+  const int64_t ngroups = n / G;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t g0 = tid; g0 < ngroups; g0 += nthr * U) {
+    T a[U][4][G], b[U][4][G];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int64_t g = g0 + u * nthr;
+      if (g < ngroups) { load_group<T, L>(v1, g, a[u]); load_group<T, L>(v2, g, b[u]); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int64_t g = g0 + u * nthr;
+      if (g < ngroups) {
+        T r[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          T x[4] = {a[u][0][j], a[u][1][j], a[u][2][j], a[u][3][j]};
+          T y[4] = {b[u][0][j], b[u][1][j], b[u][2][j], b[u][3][j]};
+          r[j] = event_mass<T, COORDS>(x, y);
+        }
+        store_group<T, G>(m, g, r);
+      }
+    }
+  }
+  if constexpr (G > 1) {
+    int64_t i = ngroups * G + tid;
+    if (i < n) {
+      T x[4], y[4];
+      load_event(v1, i, x);
+      load_event(v2, i, y);
+      m[i] = event_mass<T, COORDS>(x, y);
+    }
+  }
+}
+
+// ============================================================================
+// K2: boost by per-event (or uniform) beta
+// ============================================================================
+template <typename T, bool AOS, bool UNIFORM>
+__global__ void __launch_bounds__(256) k_boost(View4<T> v, View3<T> beta, View4o<T> out, int64_t n, T ubx,
+                                               T uby, T ubz) {
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  BoostCoef<T> ku;
+  if constexpr (UNIFORM) ku = boost_coef(ubx, uby, ubz);
+  for (int64_t i = tid; i < n; i += nthr) {
+    V4<T> x;
+    if constexpr (AOS) {
+      if constexpr (sizeof(T) == 8) {
+        double r[4];
+        ld256(reinterpret_cast<const double*>(v.c[0]) + 4 * i, r);
+        x = V4<T>{(T)r[0], (T)r[1], (T)r[2], (T)r[3]};
+      } else {
+        float4 r = __ldcs(reinterpret_cast<const float4*>(v.c[0]) + i);
+        x = V4<T>{(T)r.x, (T)r.y, (T)r.z, (T)r.w};
+      }
+    } else {
+      x = V4<T>{__ldg(v.c[0] + i * v.s), __ldg(v.c[1] + i * v.s), __ldg(v.c[2] + i * v.s), __ldg(v.c[3] + i * v.s)};
+    }
+    BoostCoef<T> k;
+    if constexpr (UNIFORM) k = ku;
+    else k = boost_coef(__ldg(beta.c[0] + i * beta.s), __ldg(beta.c[1] + i * beta.s), __ldg(beta.c[2] + i * beta.s));
+    V4<T> o = apply_boost(k, x);
+    if constexpr (AOS) {
+      if constexpr (sizeof(T) == 8) {
+        double r[4] = {(double)o.x, (double)o.y, (double)o.z, (double)o.t};
+        st256(reinterpret_cast<double*>(out.c[0]) + 4 * i, r);
+      } else {
+        __stcs(reinterpret_cast<float4*>(out.c[0]) + i, make_float4((float)o.x, (float)o.y, (float)o.z, (float)o.t));
+      }
+    } else {
+      out.c[0][i * out.s] = o.x;
+      out.c[1][i * out.s] = o.y;
+      out.c[2][i * out.s] = o.z;
+      out.c[3][i * out.s] = o.t;
+    }
+  }
+}
+
+// ============================================================================
+// K3: fused mass (lab or CM frame) + histogram, privatised in shared memory.
+// ============================================================================
+struct HistParams {
+  double lo, hi, width;  // width = hi - lo (same IEEE value the oracle forms)
+  int nbins;
+};
+
+template <typename T, int COORDS, bool CM>
+__device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], int64_t i, const View4o<T>& bo,
+                                             bool want_boosted) {
+  if constexpr (CM) {
+    V4<T> x = to_cartesian<T, COORDS>(a), y = to_cartesian<T, COORDS>(b);
+    V4<T> xa, yb;
+    T M = cm_pair_mass(x, y, &xa, &yb);
+    if (want_boosted) {
+      int64_t j0 = (2 * i) * bo.s, j1 = (2 * i + 1) * bo.s;
+      bo.c[0][j0] = xa.x; bo.c[1][j0] = xa.y; bo.c[2][j0] = xa.z; bo.c[3][j0] = xa.t;
+      bo.c[0][j1] = yb.x; bo.c[1][j1] = yb.y; bo.c[2][j1] = yb.z; bo.c[3][j1] = yb.t;
+    }
+    return M;
+  } else {
+    return event_mass<T, COORDS>(a, b);
+  }
+}
+
+template <typename T, int COORDS, int L, bool CM, bool SMEM>
+__global__ void __launch_bounds__(256) k_mass_histogram(View4<T> v1, View4<T> v2, int64_t n, HistParams hp,
+                                                        unsigned long long* __restrict__ bins, T* __restrict__ m_out,
+                                                        View4o<T> bo, bool want_boosted) {
+  extern __shared__ unsigned int sh[];
+  constexpr int G = Group<T, L>::G;
+  const int nb2 = hp.nbins + 2;
+  if constexpr (SMEM) {
+    for (int b = threadIdx.x; b < nb2; b += blockDim.x) sh[b] = 0u;
+    __syncthreads();
+  }
+  auto count = [&](T M) {
+    int b = find_bin((double)M, hp.lo, hp.hi, hp.width, hp.nbins);
+    if constexpr (SMEM) atomicAdd(&sh[b], 1u);
+    else atomicAdd(&bins[b], 1ull);
+  };
+  const int64_t ngroups = n / G;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t g = tid; g < ngroups; g += nthr) {
+    T a[4][G], b[4][G];
+    load_group<T, L>(v1, g, a);
+    load_group<T, L>(v2, g, b);
+    T r[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      T x[4] = {a[0][j], a[1][j], a[2][j], a[3][j]};
+      T y[4] = {b[0][j], b[1][j], b[2][j], b[3][j]};
+      r[j] = hist_event_mass<T, COORDS, CM>(x, y, g * G + j, bo, want_boosted);
+      count(r[j]);
+    }
+    if (m_out) store_group<T, G>(m_out, g, r);
+  }
+  if constexpr (G > 1) {
+    int64_t i = ngroups * G + tid;
+    if (i < n) {
+      T x[4], y[4];
+      load_event(v1, i, x);
+      load_event(v2, i, y);
+      T M = hist_event_mass<T, COORDS, CM>(x, y, i, bo, want_boosted);
+      count(M);
+      if (m_out) m_out[i] = M;
+    }
+  }
+  if constexpr (SMEM) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
+      unsigned int c = sh[b];
+      if (c) atomicAdd(&bins[b], (unsigned long long)c);
+    }
+  }
+}
+
+}  // namespace gvx

@@ -1,0 +1,64 @@
+"""Device twin of :mod:`synth` (libgvxsynth.so): fills CUDA tensors with the same
+events the host generator draws for the same global indices. Not the method's
+arithmetic — only the shared input generator (see synth/__init__.py)."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import DEFAULT_SEED
+
+_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgvxsynth.so")
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise ImportError(f"{_LIB} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(_LIB)
+        for f in (lib.gvx_synth_muon_pairs, lib.gvx_synth_boost_inputs):
+            f.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
+                          ctypes.c_void_p, ctypes.c_void_p]
+            f.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _code(dtype):
+    return 1 if dtype == torch.float64 else 0
+
+
+def muon_pairs(n: int, first: int = 0, seed: int = DEFAULT_SEED, dtype=torch.float64, device="cuda", out=None):
+    """(v1, v2) [n, 4] PtEtaPhiM AoS for global event indices first .. first+n-1."""
+    dev = torch.device(device)
+    if out is None:
+        v1 = torch.empty((n, 4), dtype=dtype, device=dev)
+        v2 = torch.empty((n, 4), dtype=dtype, device=dev)
+    else:
+        v1, v2 = out
+    with torch.cuda.device(dev):
+        rc = _load().gvx_synth_muon_pairs(_code(dtype), seed, first, n, v1.data_ptr(), v2.data_ptr(),
+                                          torch.cuda.current_stream(dev).cuda_stream)
+    if rc:
+        raise RuntimeError(f"gvx_synth_muon_pairs: cuda error {rc}")
+    return v1, v2
+
+
+def boost_inputs(n: int, first: int = 0, seed: int = DEFAULT_SEED, dtype=torch.float64, device="cuda", out=None):
+    """(v [n, 4] PxPyPzE, beta [n, 3]) for global event indices first .. first+n-1."""
+    dev = torch.device(device)
+    if out is None:
+        v = torch.empty((n, 4), dtype=dtype, device=dev)
+        beta = torch.empty((n, 3), dtype=dtype, device=dev)
+    else:
+        v, beta = out
+    with torch.cuda.device(dev):
+        rc = _load().gvx_synth_boost_inputs(_code(dtype), seed, first, n, v.data_ptr(), beta.data_ptr(),
+                                            torch.cuda.current_stream(dev).cuda_stream)
+    if rc:
+        raise RuntimeError(f"gvx_synth_boost_inputs: cuda error {rc}")
+    return v, beta

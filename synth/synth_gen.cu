@@ -1,0 +1,127 @@
+// synth_gen.cu — device twin of synth/__init__.py (the seeded input
+// generator shared by the oracle and the CUDA path). It holds NONE of the
+// method's arithmetic: it only draws events. Every operation mirrors the
+// numpy implementation one for one with IEEE round-to-nearest basic
+// operations and no contraction (__dadd_rn / __dmul_rn / __dsqrt_rn /
+// floor / scalbn), so host and device produce identical bits for any global
+// event index (tests/test_gpu_parity.py::test_synth_device_matches_host).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace {
+
+constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+constexpr uint32_t STREAM_V1 = 1, STREAM_V2 = 2, STREAM_BOOST_P = 3, STREAM_BOOST_BETA = 4;
+
+__device__ __forceinline__ uint4 philox(uint64_t idx, uint32_t call, uint32_t stream, uint64_t seed) {
+  uint32_t c0 = (uint32_t)idx, c1 = (uint32_t)(idx >> 32), c2 = call, c3 = stream;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
+    uint32_t hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    if (r < 9) { k0 += W0; k1 += W1; }
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ double u01(uint32_t w) {
+  return __dmul_rn(__dadd_rn((double)w, 0.5), 2.3283064365386963e-10);
+}
+__device__ __forceinline__ double normal4(uint4 w) {
+  double s = __dadd_rn(__dadd_rn(__dadd_rn(u01(w.x), u01(w.y)), u01(w.z)), u01(w.w));
+  return __dmul_rn(__dsub_rn(s, 2.0), 1.7320508075688772);
+}
+
+__constant__ double kExpCoef[14] = {
+    1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08, 2.755731922398589e-07,
+    2.7557319223985893e-06, 2.48015873015873e-05, 0.0001984126984126984, 0.001388888888888889,
+    0.008333333333333333,   0.041666666666666664, 0.16666666666666666,  0.5, 1.0, 1.0};
+
+__device__ __forceinline__ double exp_det(double x) {
+  double k = floor(__dadd_rn(__dmul_rn(x, 1.4426950408889634), 0.5));
+  double r = __dsub_rn(__dsub_rn(x, __dmul_rn(k, 0.693145751953125)), __dmul_rn(k, 1.4286068203094173e-06));
+  double p = kExpCoef[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) p = __dadd_rn(__dmul_rn(p, r), kExpCoef[i]);
+  return scalbn(p, (int)k);
+}
+
+template <typename T>
+__device__ __forceinline__ void muon(uint64_t idx, uint32_t stream, uint64_t seed, T* out) {
+  uint4 w0 = philox(idx, 0, stream, seed), w1 = philox(idx, 1, stream, seed);
+  double pt = exp_det(__dadd_rn(3.4011973816621555, __dmul_rn(0.5, normal4(w0))));
+  double eta = __dadd_rn(-2.5, __dmul_rn(5.0, u01(w1.x)));
+  double phi = __dadd_rn(-3.141592653589793, __dmul_rn(6.283185307179586, u01(w1.y)));
+  out[0] = (T)pt;
+  out[1] = (T)eta;
+  out[2] = (T)phi;
+  out[3] = (T)0.1056583755;
+}
+
+template <typename T>
+__global__ void k_muon_pairs(uint64_t seed, uint64_t first, int64_t n, T* v1, T* v2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T a[4], b[4];
+    muon<T>(first + (uint64_t)i, STREAM_V1, seed, a);
+    muon<T>(first + (uint64_t)i, STREAM_V2, seed, b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { v1[4 * i + k] = a[k]; v2[4 * i + k] = b[k]; }
+  }
+}
+
+template <typename T>
+__global__ void k_boost_inputs(uint64_t seed, uint64_t first, int64_t n, T* v, T* beta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t idx = first + (uint64_t)i;
+    double px = __dmul_rn(30.0, normal4(philox(idx, 0, STREAM_BOOST_P, seed)));
+    double py = __dmul_rn(30.0, normal4(philox(idx, 1, STREAM_BOOST_P, seed)));
+    double pz = __dmul_rn(30.0, normal4(philox(idx, 2, STREAM_BOOST_P, seed)));
+    double e = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)), __dmul_rn(pz, pz)),
+                                    0.011163692328303140));
+    double gx = normal4(philox(idx, 0, STREAM_BOOST_BETA, seed));
+    double gy = normal4(philox(idx, 1, STREAM_BOOST_BETA, seed));
+    double gz = normal4(philox(idx, 2, STREAM_BOOST_BETA, seed));
+    uint4 wm = philox(idx, 3, STREAM_BOOST_BETA, seed);
+    double mag = __dmul_rn(0.99, fmax(fmax(u01(wm.x), u01(wm.y)), u01(wm.z)));
+    double sc = __ddiv_rn(mag, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz))));
+    v[4 * i + 0] = (T)px;
+    v[4 * i + 1] = (T)py;
+    v[4 * i + 2] = (T)pz;
+    v[4 * i + 3] = (T)e;
+    beta[3 * i + 0] = (T)__dmul_rn(gx, sc);
+    beta[3 * i + 1] = (T)__dmul_rn(gy, sc);
+    beta[3 * i + 2] = (T)__dmul_rn(gz, sc);
+  }
+}
+
+int grid_of(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+}
+
+}  // namespace
+
+extern "C" {
+
+// dtype: 0 = float32, 1 = float64. v1, v2: AoS [n][4] device buffers; v: [n][4],
+// beta: [n][3]. Returns 0 or a cudaError_t value.
+int gvx_synth_muon_pairs(int dtype, uint64_t seed, uint64_t first, int64_t n, void* v1, void* v2, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == 1) k_muon_pairs<double><<<grid_of(n), 256, 0, s>>>(seed, first, n, (double*)v1, (double*)v2);
+  else k_muon_pairs<float><<<grid_of(n), 256, 0, s>>>(seed, first, n, (float*)v1, (float*)v2);
+  return (int)cudaGetLastError();
+}
+
+int gvx_synth_boost_inputs(int dtype, uint64_t seed, uint64_t first, int64_t n, void* v, void* beta, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == 1) k_boost_inputs<double><<<grid_of(n), 256, 0, s>>>(seed, first, n, (double*)v, (double*)beta);
+  else k_boost_inputs<float><<<grid_of(n), 256, 0, s>>>(seed, first, n, (float*)v, (float*)beta);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"

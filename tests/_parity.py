@@ -1,0 +1,104 @@
+"""Parity predicates shared by the GPU tests (test infrastructure only).
+
+Tolerances are the north star's (BASELINE.json): |ΔM²| ≤ τ·E² and
+component-wise |Δ| ≤ τ·E, τ = 1e-12 (f64) / 1e-5 (f32), with the scales of
+DESIGN.md reading R5 (E_lab for masses, S = γ(E + |β||p|) for boosts), and the
+histogram exemption rule of reading R14.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+TAU = {np.dtype(np.float64): 1e-12, np.dtype(np.float32): 1e-5}
+
+
+def tau_of(dtype) -> float:
+    return TAU[np.dtype(dtype)]
+
+
+def mass_violations(m_gpu, m_ref, e_lab, tau):
+    """Indices where the GPU mass breaks |M_g|M_g| − M_o|M_o|| ≤ τ·E_lab², or where
+    exactly one side is non-finite."""
+    g = np.asarray(m_gpu, np.float64)
+    o = np.asarray(m_ref, np.float64)
+    e = np.asarray(e_lab, np.float64)
+    fin_g, fin_o = np.isfinite(g), np.isfinite(o)
+    bad = fin_g != fin_o
+    both = fin_g & fin_o
+    with np.errstate(invalid="ignore", over="ignore"):
+        err = np.abs(g * np.abs(g) - o * np.abs(o))
+        lim = tau * e * e
+    bad |= both & ~(err <= lim)
+    return np.nonzero(bad)[0]
+
+
+def boost_violations(out_gpu, out_ref, scale, tau):
+    g = np.asarray(out_gpu, np.float64)
+    o = np.asarray(out_ref, np.float64)
+    s = np.asarray(scale, np.float64)
+    fin_g, fin_o = np.isfinite(g), np.isfinite(o)
+    bad = (fin_g != fin_o).any(axis=1)
+    with np.errstate(invalid="ignore"):
+        err = np.where(fin_g & fin_o, np.abs(g - o), 0.0).max(axis=1)
+    bad |= ~(err <= tau * np.where(np.isfinite(s), s, np.inf))
+    return np.nonzero(bad)[0]
+
+
+def find_bin_np(x, lo, hi, nbins):
+    """Vectorised ROOT FindFixBin in double (same operation order as the oracle)."""
+    x = np.asarray(x, np.float64)
+    with np.errstate(invalid="ignore"):
+        q = (float(nbins) * (x - lo)) / (hi - lo)
+        inner = 1 + np.trunc(np.where(np.isfinite(q), q, 0)).astype(np.int64)
+    b = np.where(x < lo, 0, np.where(~(x < hi), nbins + 1, inner))
+    return b.astype(np.int64)
+
+
+def hist_check(h_gpu, m_ref, e_lab, tau, lo, hi, nbins, nan_possible=None, m_window_center=None):
+    """Reading R14. Returns a list of failure strings (empty = pass).
+
+    δ_i = τ·E_i² / max(|M_i|, √τ·E_i); event i is ambiguous if an edge of the axis lies
+    within δ_i of its oracle mass M_i. h_s = oracle histogram of non-ambiguous events.
+    Require h_gpu ≥ h_s bin-wise, Σ(h_gpu − h_s) = #ambiguous, and each bin's excess
+    ≤ #ambiguous events whose window [M−δ, M+δ] touches it (events flagged in
+    ``nan_possible`` may also land in the overflow bin; their window is centred on
+    ``m_window_center`` — the lab mass — when the oracle's own mass is NaN)."""
+    h_gpu = np.asarray(h_gpu, np.int64)
+    m = np.asarray(m_ref, np.float64).copy()
+    e = np.asarray(e_lab, np.float64)
+    n = m.size
+    nanp = np.zeros(n, bool) if nan_possible is None else np.asarray(nan_possible, bool)
+    if m_window_center is not None:
+        c = np.asarray(m_window_center, np.float64)
+        m = np.where(np.isnan(m) & nanp, c, m)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        delta = tau * e * e / np.maximum(np.abs(m), np.sqrt(tau) * e)
+    w = (hi - lo) / nbins
+    fin = np.isfinite(m)
+    with np.errstate(invalid="ignore"):
+        k = np.clip(np.round((m - lo) / w), 0, nbins)
+        nearest_edge = lo + k * w
+        amb = fin & (np.abs(m - nearest_edge) <= delta + 1e-12 * np.abs(m)) & (m > lo - delta - w) & (m < hi + delta + w)
+    amb |= nanp
+    b_ref = find_bin_np(np.asarray(m_ref, np.float64), lo, hi, nbins)
+    h_s = np.bincount(b_ref[~amb], minlength=nbins + 2).astype(np.int64)
+    fails = []
+    if (h_gpu < h_s).any():
+        bad = np.nonzero(h_gpu < h_s)[0][:10]
+        fails.append(f"bins below the unambiguous oracle count: {bad.tolist()}")
+    excess = h_gpu - h_s
+    if excess.sum() != amb.sum():
+        fails.append(f"total excess {excess.sum()} != #ambiguous {amb.sum()}")
+    allowed = np.zeros(nbins + 2, np.int64)
+    idx = np.nonzero(amb)[0]
+    for i in idx:
+        if np.isfinite(m[i]):
+            b0 = find_bin_np(m[i] - delta[i], lo, hi, nbins)
+            b1 = find_bin_np(m[i] + delta[i], lo, hi, nbins)
+            allowed[int(b0):int(b1) + 1] += 1
+        if nanp[i] or not np.isfinite(m[i]):
+            allowed[nbins + 1] += 1
+    if (excess > allowed).any():
+        bad = np.nonzero(excess > allowed)[0][:10]
+        fails.append(f"bins exceed their ambiguous allowance: {bad.tolist()}")
+    return fails, int(amb.sum())

@@ -1,0 +1,365 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element, on the same seeded inputs. Run on a B200 with ``pytest -m gpu``.
+
+Inputs come from synth (host generator for the oracle; its bit-identical device
+twin for large batches). No expected value here is produced by the CUDA path.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from tests._parity import boost_violations, find_bin_np, hist_check, mass_violations, tau_of
+
+pytestmark = pytest.mark.gpu
+
+LO, HI, NB = 0.25, 300.0, 1000
+TDT = {np.float32: torch.float32, np.float64: torch.float64}
+
+
+@pytest.fixture(scope="module")
+def gvx():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2312_02756_b200 as g
+    return g
+
+
+@pytest.fixture(scope="module")
+def O(oracle_lib):
+    return oracle_lib
+
+
+def dev(a, dt=None):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def edge_events(dt):
+    """Hand-built PtEtaPhiM pairs covering the degenerate cases of the method."""
+    inf, nan = np.inf, np.nan
+    rows = [
+        # (v1, v2)
+        ([30, 0.5, 1.0, 0.105], [0, 0, 0, 0]),                # single vector → m
+        ([1, 0, 0, -0.5], [0, 0, 0, 0]),                      # spacelike, negative mass convention
+        ([1, 0, 0, -5.0], [2, 0.3, 0.1, -3.0]),               # E² clamp on both (R2)
+        ([25, 1.1, 0.3, 0], [25, -1.1, 0.3 - np.pi, 0]),      # back-to-back massless
+        ([20, 2.4, -3.0, 0.105], [20, 2.39, -3.01, 0.105]),   # near-collinear
+        ([40, 0.0, 0.0, 0.105], [40, 0.0, 0.0, 0.105]),       # exactly collinear
+        ([50, 25.0, 0.2, 0.105], [30, -1.0, 2.0, 0.105]),     # |η| beyond the fast domain (cold path)
+        ([50, -30.0, 0.2, 0.105], [30, 40.0, 2.0, 0.105]),
+        ([50, 1.0, 1e5, 0.105], [30, -1.0, -2e5, 0.105]),     # |φ| ≫ π (R16)
+        ([50, 1.0, 7.5, 0.105], [30, -1.0, -7.9, 0.105]),     # φ just outside (−π, π]
+        ([0, 0, 0, 91.0], [0, 0, 0, 0.0]),                    # at rest
+        ([0, 0, 0, 0], [0, 0, 0, 0]),                         # all zero
+        ([nan, 0, 0, 0.1], [3, 0, 0, 0.1]),                   # NaN propagates
+        ([3, 0, 0, 0.1], [3, inf, 0, 0.1]),                   # Inf
+        ([1e3, 2.5, -3.1, 0.105], [2e3, -2.5, 3.1, 0.105]),   # high pt, edges of acceptance
+        ([5, 0.3, 1.0, 10.0], [7, -0.2, -1.0, 80.0]),         # heavy
+    ]
+    a = np.array([r[0] for r in rows], np.float64).astype(dt)
+    b = np.array([r[1] for r in rows], np.float64).astype(dt)
+    return a, b
+
+
+def mixed_inputs(n, dt, seed=12345, first=0):
+    v1, v2 = synth.muon_pairs(np.arange(first, first + n), seed=seed, dtype=dt)
+    ea, eb = edge_events(dt)
+    v1 = np.concatenate([ea, v1, ea])
+    v2 = np.concatenate([eb, v2, eb])
+    return v1, v2
+
+
+# ----------------------------------------------------------------------------
+# generator twin
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("first", [0, 700_000_123])
+def test_synth_device_matches_host(dt, first):
+    import synth.device as sd
+    n = 50_001
+    v1d, v2d = sd.muon_pairs(n, first=first, dtype=TDT[dt])
+    v1h, v2h = synth.muon_pairs(np.arange(first, first + n), dtype=dt)
+    assert np.array_equal(host(v1d), v1h) and np.array_equal(host(v2d), v2h)
+    vd, bd = sd.boost_inputs(n, first=first, dtype=TDT[dt])
+    vh, bh = synth.boost_inputs(np.arange(first, first + n), dtype=dt)
+    assert np.array_equal(host(vd), vh) and np.array_equal(host(bd), bh)
+
+
+# ----------------------------------------------------------------------------
+# K1 invariant mass
+# ----------------------------------------------------------------------------
+
+def test_cfg1_mass_65536_f64(gvx, O):
+    """BASELINE configs[0]: N = 65536 PtEtaPhiM pairs, fp64, AoS, vs the oracle."""
+    v1, v2 = synth.muon_pairs(np.arange(65536), dtype=np.float64)
+    m = host(gvx.invariant_mass(dev(v1), dev(v2)))
+    mo, e = O.invariant_mass(v1, v2)
+    bad = mass_violations(m, mo, e, 1e-12)
+    assert bad.size == 0, (bad[:5], m[bad[:5]], mo[bad[:5]])
+    rel = np.abs(m * np.abs(m) - mo * np.abs(mo)) / e ** 2
+    print(f"cfg1 max |dM2|/E2 = {rel.max():.3e}")
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("coords", ["ptetaphim", "pxpypze"])
+def test_mass_parity_layouts(gvx, O, dt, coords):
+    n = 3 * 256 * 148 + 37  # several tiles per CTA + a ragged tail
+    v1, v2 = mixed_inputs(n, dt)
+    if coords == "pxpypze":
+        # Cartesian inputs: the boost generator's on-shell vectors, plus the edge rows as given
+        a, _ = synth.boost_inputs(np.arange(v1.shape[0]), dtype=dt, seed=5)
+        b, _ = synth.boost_inputs(np.arange(v1.shape[0]), dtype=dt, seed=6)
+        v1, v2 = a, b
+    mo, e = O.invariant_mass(v1, v2, coords=coords)
+    tau = tau_of(dt)
+    t1, t2 = dev(v1), dev(v2)
+    m_aos = host(gvx.invariant_mass(t1, t2, coords=coords))
+    bad = mass_violations(m_aos, mo, e, tau)
+    assert bad.size == 0, (bad[:8], m_aos[bad[:8]], mo[bad[:8]])
+    # SoA: 4 separate component arrays
+    s1 = [t1[:, k].contiguous() for k in range(4)]
+    s2 = [t2[:, k].contiguous() for k in range(4)]
+    m_soa = host(gvx.invariant_mass(s1, s2, coords=coords))
+    # interleaved pairs [N, 2, 4] (strided view, stride 8)
+    pairs = torch.stack([t1, t2], dim=1).contiguous()
+    m_pair = host(gvx.invariant_mass(pairs[:, 0, :], pairs[:, 1, :], coords=coords))
+    # misaligned AoS view (offset by one vector: 16/32-byte alignment lost for f32/f64)
+    big1 = torch.cat([t1[:1], t1]).contiguous()[1:]
+    big2 = torch.cat([t2[:1], t2]).contiguous()[1:]
+    m_mis = host(gvx.invariant_mass(big1, big2, coords=coords))
+    for other in (m_soa, m_pair, m_mis):
+        assert np.array_equal(other, m_aos, equal_nan=True)  # bitwise identical across layouts
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_mass_small_and_empty(gvx, O, dt):
+    for n in (0, 1, 2, 3, 5, 7, 9, 255, 257):
+        v1, v2 = synth.muon_pairs(np.arange(n), dtype=dt)
+        mo, e = O.invariant_mass(v1, v2)
+        m = host(gvx.invariant_mass(dev(v1).reshape(n, 4), dev(v2).reshape(n, 4)))
+        assert m.shape == (n,)
+        assert mass_violations(m, mo, e, tau_of(dt)).size == 0
+
+
+def test_mass_errors(gvx):
+    a = torch.zeros((4, 4), device="cuda")
+    with pytest.raises(ValueError):
+        gvx.invariant_mass(a, torch.zeros((5, 4), device="cuda"))
+    with pytest.raises(ValueError):
+        gvx.invariant_mass(a.cpu(), a.cpu())
+    with pytest.raises(TypeError):
+        gvx.invariant_mass(a.half(), a.half())
+
+
+# ----------------------------------------------------------------------------
+# K2 boost
+# ----------------------------------------------------------------------------
+
+def boost_edge_rows(dt):
+    v = np.array([[0, 0, 0, 1.0], [1, 2, 3, 10], [3, 0, 4, 5], [0, 0, 0, 0], [5, -7, 9, 30]], np.float64)
+    b = np.array([[0, 0, 0.6], [0, 0, 0], [0.9, 0.9, 0], [0.5, -0.5, 0.5], [np.nan, 0, 0]], np.float64)
+    return v.astype(dt), b.astype(dt)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_boost_parity(gvx, O, dt):
+    n = 2 * 256 * 148 + 11
+    v, b = synth.boost_inputs(np.arange(n), dtype=dt)
+    ev, eb = boost_edge_rows(dt)
+    v = np.concatenate([ev, v])
+    b = np.concatenate([eb, b])
+    ref, s = O.boost(v, b)
+    tv, tb = dev(v), dev(b)
+    out = host(gvx.boost(tv, tb))
+    bad = boost_violations(out, ref, s, tau_of(dt))
+    assert bad.size == 0, (bad[:5], out[bad[:5]], ref[bad[:5]])
+    # SoA and in-place give the same bits
+    out_soa = gvx.boost([tv[:, k].contiguous() for k in range(4)], [tb[:, k].contiguous() for k in range(3)])
+    assert np.array_equal(np.stack([host(c) for c in out_soa], 1), out, equal_nan=True)
+    tv2 = tv.clone()
+    gvx.boost(tv2, tb, out=tv2)
+    assert np.array_equal(host(tv2), out, equal_nan=True)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_boost_uniform_parity(gvx, O, dt):
+    v, _ = synth.boost_inputs(np.arange(100_003), dtype=dt)
+    beta = (0.3, -0.4, 0.5)
+    ref = O.boost_uniform(v, *[dt(x) for x in beta])
+    out = host(gvx.boost_uniform(dev(v), beta))
+    s = O.boost(v, np.tile(np.array(beta, dt), (v.shape[0], 1)))[1]
+    assert boost_violations(out, ref, s, tau_of(dt)).size == 0
+    with pytest.raises(gvx.DomainError):
+        gvx.boost_uniform(dev(v), (0.9, 0.9, 0.0))
+
+
+def test_boost_inverse_on_gpu(gvx):
+    """β then −β recovers the input at 2^20 events: |Δ| ≤ τ·(S + γS'),
+    bounded here by τ·4γ²E."""
+    import synth.device as sd
+    v, b = sd.boost_inputs(1 << 20)
+    back = gvx.boost(gvx.boost(v, b), -b)
+    g = 1 / torch.sqrt(1 - (b * b).sum(1))
+    err = ((back - v).abs().max(1).values / (4 * g * g * v[:, 3])).max().item()
+    assert err <= 1e-12
+
+
+# ----------------------------------------------------------------------------
+# K3 fused histogram (lab and CM)
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("cm", [False, True])
+def test_histogram_parity(gvx, O, dt, cm):
+    n = 200_003
+    v1, v2 = mixed_inputs(n, dt, seed=99)
+    bins_o, mo = O.mass_histogram(v1, v2, LO, HI, NB, cm=cm)
+    mlab, e = O.invariant_mass(v1, v2)
+    t1, t2 = dev(v1), dev(v2)
+    m_out = torch.empty(v1.shape[0], dtype=TDT[dt], device="cuda")
+    bo = torch.empty((2 * v1.shape[0], 4), dtype=TDT[dt], device="cuda") if cm else None
+    h = host(gvx.mass_histogram(t1, t2, LO, HI, NB, cm=cm, m_out=m_out, boosted_out=bo))
+    assert h.sum() == v1.shape[0]
+    tau = tau_of(dt)
+    mg = host(m_out)
+    if cm:
+        # CM NaN is possible where β_cm² rounds to 1: near-collinear pairs (reading R11/R14)
+        nanp = np.isnan(mo) | (np.abs(mlab.astype(np.float64)) < (1e-2 if dt == np.float32 else 1e-6) * e)
+        fails, namb = hist_check(h, mo, e, tau, LO, HI, NB, nan_possible=nanp, m_window_center=mlab)
+        ok = ~nanp
+        bad = mass_violations(mg[ok], mo[ok], e[ok], tau)
+        assert bad.size == 0
+    else:
+        fails, namb = hist_check(h, mo, e, tau, LO, HI, NB)
+        assert mass_violations(mg, mo, e, tau).size == 0
+        # the fused kernel's mass equals the mass kernel's, bit for bit
+        assert np.array_equal(mg, host(gvx.invariant_mass(t1, t2)), equal_nan=True)
+    assert not fails, fails
+    # the GPU's own bins agree exactly with binning its masses
+    assert np.array_equal(h, np.bincount(find_bin_np(mg, LO, HI, NB), minlength=NB + 2))
+    print(f"hist dt={dt.__name__} cm={cm}: ambiguous events {namb}, exact bins "
+          f"{int((h == bins_o).sum())}/{NB + 2}")
+    if cm and dt == np.float64:
+        _, _, bref = O.cm_mass(v1, v2, want_boosted=True)
+        bg = host(bo).reshape(-1, 8)
+        fin = np.isfinite(bref).all(1)
+        S = e[fin] ** 2 / np.maximum(np.abs(mlab[fin]), 1e-300)
+        err = np.abs(bg[fin] - bref[fin]).max(1) / S
+        assert err.max() <= 1e-12
+
+
+def test_histogram_accumulates_and_shards(gvx):
+    import synth.device as sd
+    n = 1 << 21
+    v1, v2 = sd.muon_pairs(n, dtype=torch.float32)
+    full = gvx.mass_histogram(v1, v2)
+    acc = gvx.new_bins()
+    for r in range(8):
+        a, b = synth.shard_range(n, r, 8)
+        gvx.mass_histogram(v1[a:b], v2[a:b], bins=acc)
+    assert torch.equal(full, acc)
+    gvx.mass_histogram(v1, v2, bins=acc)
+    assert torch.equal(acc, 2 * full)
+
+
+def test_histogram_single_bin_and_specials(gvx, O):
+    # every pair at rest with mass 91 → one bin (contention stress)
+    v = torch.zeros((1 << 20, 4), dtype=torch.float64, device="cuda")
+    v[:, 3] = 45.5
+    h = host(gvx.mass_histogram(v, v, coords="pxpypze"))
+    b = find_bin_np(np.array([91.0]), LO, HI, NB)[0]
+    assert h[b] == 1 << 20 and h.sum() == 1 << 20
+    # NaN → overflow, exact lower edge → bin 1, M = hi → overflow, negative → underflow
+    rows = np.array([[np.nan, 0, 0, 1], [0, 0, 0, LO / 2], [0, 0, 0, HI / 2], [1, 0, 0, 0.0]], np.float64)
+    rows2 = np.array([[0, 0, 0, 1], [0, 0, 0, LO / 2], [0, 0, 0, HI / 2], [-1, 0, 0, 0.0]], np.float64)
+    hg = host(gvx.mass_histogram(dev(rows), dev(rows2), coords="pxpypze"))
+    ho, _ = O.mass_histogram(rows, rows2, LO, HI, NB, coords="pxpypze")
+    assert np.array_equal(hg, ho.astype(np.int64))
+    assert hg[NB + 1] == 2 and hg[1] == 1
+
+
+def test_histogram_nbins_variants(gvx, O):
+    v1, v2 = synth.muon_pairs(np.arange(50_000), dtype=np.float64)
+    for lo, hi, nb in ((0.0, 200.0, 1), (0.0, 200.0, 7), (-50.0, 50.0, 100_000)):
+        ho, mo = O.mass_histogram(v1, v2, lo, hi, nb)
+        _, e = O.invariant_mass(v1, v2)
+        h = host(gvx.mass_histogram(dev(v1), dev(v2), lo, hi, nb))
+        fails, _ = hist_check(h, mo, e, 1e-12, lo, hi, nb)
+        assert not fails, (lo, hi, nb, fails)
+    with pytest.raises(gvx.GvxError):
+        gvx.mass_histogram(dev(v1), dev(v2), 1.0, 1.0, 10)
+
+
+# ----------------------------------------------------------------------------
+# Full-size configurations, launched as bench.py launches them: sampled outputs
+# ----------------------------------------------------------------------------
+
+def _sample_idx(n, k=4096, seed=0):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([rng.integers(0, n, k), [0, n - 1]]))
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_cfg2_mass_1e8_sampled(gvx, O, dt):
+    import synth.device as sd
+    n = 100_000_000
+    v1, v2 = sd.muon_pairs(n, dtype=TDT[dt])
+    m = gvx.invariant_mass(v1, v2)
+    idx = _sample_idx(n)
+    a, b = synth.muon_pairs(idx, dtype=dt)
+    mo, e = O.invariant_mass(a, b)
+    mg = host(m[torch.from_numpy(idx).cuda()])
+    assert mass_violations(mg, mo, e, tau_of(dt)).size == 0
+    # SoA at full size on the same events
+    del m
+    s1 = [v1[:, k].contiguous() for k in range(4)]
+    del v1
+    s2 = [v2[:, k].contiguous() for k in range(4)]
+    del v2
+    m = gvx.invariant_mass(s1, s2)
+    assert mass_violations(host(m[torch.from_numpy(idx).cuda()]), mo, e, tau_of(dt)).size == 0
+
+
+def test_cfg3_boost_1e8_sampled(gvx, O):
+    import synth.device as sd
+    n = 100_000_000
+    v, b = sd.boost_inputs(n, dtype=torch.float64)
+    out = gvx.boost(v, b)
+    idx = _sample_idx(n, seed=1)
+    vh, bh = synth.boost_inputs(idx, dtype=np.float64)
+    ref, s = O.boost(vh, bh)
+    assert boost_violations(host(out[torch.from_numpy(idx).cuda()]), ref, s, 1e-12).size == 0
+
+
+@pytest.mark.parametrize("cm", [False, True])
+def test_cfg4_cfg5_histogram_1e9_f32(gvx, O, cm):
+    """configs[3]/[4] at full size on one GPU: 1e9 fp32 pairs; masses sampled vs the
+    oracle, bins vs sharded (8 shards) accumulation, bitwise."""
+    import synth.device as sd
+    n = 1_000_000_000
+    v1, v2 = sd.muon_pairs(n, dtype=torch.float32)
+    m_out = torch.empty(n, dtype=torch.float32, device="cuda")
+    h = gvx.mass_histogram(v1, v2, cm=cm, m_out=m_out)
+    assert int(h.sum()) == n
+    acc = gvx.new_bins()
+    for r in range(8):
+        a, b = synth.shard_range(n, r, 8)
+        gvx.mass_histogram(v1[a:b], v2[a:b], cm=cm, bins=acc)
+    assert torch.equal(h, acc)
+    idx = _sample_idx(n, seed=2)
+    a, b = synth.muon_pairs(idx, dtype=np.float32)
+    mo, e = (O.cm_mass(a, b) if cm else O.invariant_mass(a, b))
+    mlab, _ = O.invariant_mass(a, b)
+    mg = host(m_out[torch.from_numpy(idx).cuda()])
+    ok = np.isfinite(mo) & (np.abs(mlab) >= 1e-2 * e) if cm else np.ones(idx.size, bool)
+    assert mass_violations(mg[ok], mo[ok], e[ok], 1e-5).size == 0
+    # the bins are exactly FindBin (double, oracle order) of the kernel's own masses
+    x = m_out.double()
+    q = (float(NB) * (x - LO)) / (HI - LO)
+    inner = 1 + torch.trunc(torch.nan_to_num(q, nan=0.0, posinf=0.0, neginf=0.0)).long()
+    b = torch.where(x < LO, 0, torch.where(~(x < HI), NB + 1, inner))
+    assert torch.equal(torch.bincount(b, minlength=NB + 2), h)

@@ -1,0 +1,52 @@
+"""The shared input generator: determinism, index addressing (any subset of a
+batch regenerates identically — the property sampled full-size parity relies
+on), and the distribution recipe of DESIGN.md §4."""
+import numpy as np
+
+import synth
+
+
+def test_philox_known_answer():
+    # Random123 known-answer vectors for Philox4x32-10
+    r = synth.philox4x32(np.array([0], np.uint64), np.array([0], np.uint64), np.array([0], np.uint64),
+                         np.array([0], np.uint64), 0, 0)
+    assert [int(x[0]) for x in r] == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    ff = np.array([0xFFFFFFFF], np.uint64)
+    r = synth.philox4x32(ff, ff, ff, ff, 0xFFFFFFFF, 0xFFFFFFFF)
+    assert [int(x[0]) for x in r] == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+
+
+def test_subset_regeneration_and_determinism():
+    full1, full2 = synth.muon_pairs(np.arange(5000))
+    idx = np.array([4999, 17, 0, 2500])
+    s1, s2 = synth.muon_pairs(idx)
+    assert np.array_equal(s1, full1[idx]) and np.array_equal(s2, full2[idx])
+    again, _ = synth.muon_pairs(np.arange(5000))
+    assert np.array_equal(again, full1)
+    other, _ = synth.muon_pairs(np.arange(5000), seed=1)
+    assert not np.array_equal(other, full1)
+
+
+def test_distribution_recipe():
+    v1, v2 = synth.muon_pairs(np.arange(200_000))
+    for v in (v1, v2):
+        pt, eta, phi, m = v.T
+        assert 20 < np.median(pt) < 40 and pt.min() > 2 and pt.max() < 2000
+        assert np.abs(np.log(pt).std() - 0.5) < 0.01
+        assert np.abs(eta).max() < 2.5 and abs(eta.mean()) < 0.02
+        assert phi.min() >= -np.pi and phi.max() < np.pi
+        assert np.all(m == synth.MUON_MASS)
+    v, b = synth.boost_inputs(np.arange(200_000))
+    bm = np.sqrt((b ** 2).sum(1))
+    assert bm.max() < 0.99
+    # |β| = 0.99·u^(1/3): P(|β| < 0.99/2) = 1/8
+    assert abs((bm < 0.495).mean() - 0.125) < 0.005
+    assert np.abs(b.mean(0)).max() < 0.01
+    assert np.allclose(v[:, 3] ** 2 - (v[:, :3] ** 2).sum(1), synth.MUON_MASS2, atol=1e-9 * v[:, 3].max() ** 2)
+    f32, _ = synth.muon_pairs(np.arange(100), dtype=np.float32)
+    assert f32.dtype == np.float32 and np.array_equal(f32, v1[:100].astype(np.float32))
+
+
+def test_exp_det_accuracy():
+    x = np.linspace(-30, 30, 200001)
+    assert np.max(np.abs(synth._exp_det(x) / np.exp(x) - 1)) < 1e-15
