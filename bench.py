@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample", type=int, default=1 << 21, help="events in the oracle's bounded sample")
+    p.add_argument("--cpu-sample", type=int, default=1 << 22, help="events in the oracle's bounded sample")
     return p.parse_args()
 
 

@@ -16,6 +16,25 @@ def tau_of(dtype) -> float:
     return TAU[np.dtype(dtype)]
 
 
+def energy_scale(O, v1, v2, coords="ptetaphim"):
+    """Reading R5: the "E" of |ΔM²| ≤ τ·E² is Σ_i max(E_i, |p_i|) — equal to the oracle's
+    E_lab = E1 + E2 for every timelike or lightlike vector, and the right rounding scale
+    for spacelike inputs whose E² the conversion clamps to 0 (R2)."""
+    z = np.zeros_like(v1)
+    _, e1 = O.invariant_mass(v1, z, coords=coords)
+    _, e2 = O.invariant_mass(v2, z, coords=coords)
+    a = np.asarray(v1, np.float64)
+    b = np.asarray(v2, np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        if coords == "ptetaphim":
+            p1 = np.abs(a[:, 0]) * np.cosh(a[:, 1])
+            p2 = np.abs(b[:, 0]) * np.cosh(b[:, 1])
+        else:
+            p1 = np.sqrt((a[:, :3] ** 2).sum(1))
+            p2 = np.sqrt((b[:, :3] ** 2).sum(1))
+        return np.fmax(e1.astype(np.float64), p1) + np.fmax(e2.astype(np.float64), p2)
+
+
 def mass_violations(m_gpu, m_ref, e_lab, tau):
     """Indices where the GPU mass breaks |M_g|M_g| − M_o|M_o|| ≤ τ·E_lab², or where
     exactly one side is non-finite."""

@@ -9,7 +9,7 @@ import pytest
 import torch
 
 import synth
-from tests._parity import boost_violations, find_bin_np, hist_check, mass_violations, tau_of
+from tests._parity import boost_violations, energy_scale, find_bin_np, hist_check, mass_violations, tau_of
 
 pytestmark = pytest.mark.gpu
 
@@ -114,7 +114,8 @@ def test_mass_parity_layouts(gvx, O, dt, coords):
         a, _ = synth.boost_inputs(np.arange(v1.shape[0]), dtype=dt, seed=5)
         b, _ = synth.boost_inputs(np.arange(v1.shape[0]), dtype=dt, seed=6)
         v1, v2 = a, b
-    mo, e = O.invariant_mass(v1, v2, coords=coords)
+    mo, _ = O.invariant_mass(v1, v2, coords=coords)
+    e = energy_scale(O, v1, v2, coords)
     tau = tau_of(dt)
     t1, t2 = dev(v1), dev(v2)
     m_aos = host(gvx.invariant_mass(t1, t2, coords=coords))
@@ -178,7 +179,8 @@ def test_boost_parity(gvx, O, dt):
     bad = boost_violations(out, ref, s, tau_of(dt))
     assert bad.size == 0, (bad[:5], out[bad[:5]], ref[bad[:5]])
     # SoA and in-place give the same bits
-    out_soa = gvx.boost([tv[:, k].contiguous() for k in range(4)], [tb[:, k].contiguous() for k in range(3)])
+    out_soa = [torch.empty(tv.shape[0], dtype=tv.dtype, device="cuda") for _ in range(4)]
+    gvx.boost([tv[:, k].contiguous() for k in range(4)], [tb[:, k].contiguous() for k in range(3)], out=out_soa)
     assert np.array_equal(np.stack([host(c) for c in out_soa], 1), out, equal_nan=True)
     tv2 = tv.clone()
     gvx.boost(tv2, tb, out=tv2)
@@ -218,7 +220,8 @@ def test_histogram_parity(gvx, O, dt, cm):
     n = 200_003
     v1, v2 = mixed_inputs(n, dt, seed=99)
     bins_o, mo = O.mass_histogram(v1, v2, LO, HI, NB, cm=cm)
-    mlab, e = O.invariant_mass(v1, v2)
+    mlab, _ = O.invariant_mass(v1, v2)
+    e = energy_scale(O, v1, v2)
     t1, t2 = dev(v1), dev(v2)
     m_out = torch.empty(v1.shape[0], dtype=TDT[dt], device="cuda")
     bo = torch.empty((2 * v1.shape[0], 4), dtype=TDT[dt], device="cuda") if cm else None
