@@ -27,7 +27,8 @@ from typing import Optional, Sequence, Union
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgvx.so")
+# GVX_LIB may point at the tuning build (tools/libgvx_tune.so) for A/B runs.
+LIB_PATH = os.environ.get("GVX_LIB") or os.path.join(_PKG, "libgvx.so")
 
 GVX_OK = 0
 GVX_ERR_INVALID_ARGUMENT = 1

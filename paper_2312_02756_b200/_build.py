@@ -19,8 +19,15 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-
 TARGETS = {
     os.path.join(PKG, "libgvx.so"): {
         "main": os.path.join(PKG, "csrc", "gvx_api.cu"),
-        "deps": [os.path.join(PKG, "csrc", f) for f in ("gvx_api.cu", "gvx_kernels.cuh", "gvx_math.cuh")]
+        "deps": [os.path.join(PKG, "csrc", f) for f in ("gvx_api.cu", "gvx_kernels.cuh", "gvx_math.cuh", "gvx_tma.cuh")]
         + [os.path.join(ROOT, "include", "gvx.h")],
+    },
+    os.path.join(ROOT, "tools", "libgvx_tune.so"): {
+        "main": os.path.join(PKG, "csrc", "gvx_api.cu"),
+        "deps": [os.path.join(PKG, "csrc", f) for f in ("gvx_api.cu", "gvx_kernels.cuh", "gvx_math.cuh", "gvx_tma.cuh")]
+        + [os.path.join(ROOT, "include", "gvx.h")],
+        "extra": ["-DGVX_TUNE"],
+        "optional": True,
     },
     os.path.join(ROOT, "synth", "libgvxsynth.so"): {
         "main": os.path.join(ROOT, "synth", "synth_gen.cu"),
@@ -36,11 +43,15 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> None:
+def build(force: bool = False, verbose: bool = False, tune: bool = False) -> None:
+    """Build the product libraries; ``tune=True`` also builds tools/libgvx_tune.so (the
+    same sources with -DGVX_TUNE: extra kernel variants for A/B measurements)."""
     for out, spec in TARGETS.items():
+        if spec.get("optional") and not tune:
+            continue
         if not force and not _stale(out, spec["deps"]):
             continue
-        cmd = [NVCC] + COMMON + ["-o", out + ".tmp", spec["main"]]
+        cmd = [NVCC] + COMMON + spec.get("extra", []) + ["-o", out + ".tmp", spec["main"]]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
@@ -48,4 +59,5 @@ def build(force: bool = False, verbose: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    import sys
+    build(force=True, verbose=True, tune="--tune" in sys.argv)

@@ -2,11 +2,14 @@
 // kernel selection and persistent-grid launch. No allocation, no host sync.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 
 #include "../../include/gvx.h"
 #include "gvx_kernels.cuh"
@@ -37,13 +40,38 @@ int sm_count() {
   return sms;
 }
 
+// Per (kernel, device, dynamic smem) occupancy, queried once and cached
+// (mutex-protected; host-side only). Also raises the kernel's dynamic shared
+// memory limit the first time a size above 48 KB is requested.
+std::mutex g_occ_mu;
+std::map<std::tuple<const void*, int, size_t, int>, int> g_occ;
+
+template <typename K>
+int blocks_per_sm(K kernel, int block, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto key = std::make_tuple((const void*)kernel, dev, smem, block);
+  {
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+  }
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 0;
+  cudaGetLastError();
+  std::lock_guard<std::mutex> lk(g_occ_mu);
+  g_occ[key] = per_sm;
+  return per_sm;
+}
+
 // Persistent grid: enough CTAs to fill every SM at the kernel's occupancy,
 // never more than the work needs.
 template <typename K>
 int grid_for(K kernel, int block, size_t smem, int64_t work_items_per_block_pass, int64_t items) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
+  int per_sm = blocks_per_sm(kernel, block, smem);
+  if (per_sm < 1) per_sm = 1;
   int64_t full = (int64_t)sm_count() * per_sm;
   int64_t need = (items + work_items_per_block_pass - 1) / work_items_per_block_pass;
   if (need < 1) need = 1;
@@ -104,12 +132,108 @@ View3<T> mk3(const gvx_vec3_cview* v) {
 
 constexpr int kBlock = 256;
 
+// GVX_DISABLE_TMA=1 routes AoS pairs to the LDG kernels (A/B measurements).
+bool tma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GVX_DISABLE_TMA");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+// Which AoS pair kernels take the TMA ring by default. Measured on B200
+// (profiles/r01/sweep_f64_variants.jsonl, bench_{tma,ldg}_*.jsonl): the ring
+// wins only for the f32 CM histogram; the f64 kernels are FP64/issue-bound and
+// do better with the register-resident LDG kernels at higher occupancy.
+// GVX_FORCE_TMA=1 routes every AoS pair kernel through the ring.
+template <typename T, int MODE>
+bool tma_preferred() {
+  static const bool force = [] {
+    const char* e = getenv("GVX_FORCE_TMA");
+    return e && e[0] == '1';
+  }();
+  return force || (sizeof(T) == 4 && MODE == PM_HIST_CM);
+}
+
+// ------------------------------------------------------- TMA pair stream ----
+template <typename T> struct TmaCfgOf;
+template <> struct TmaCfgOf<double> { using type = PairTma<double, 512, 3, 8>; };
+template <> struct TmaCfgOf<float> { using type = PairTma<float, 512, 4, 8>; };
+
+#ifdef GVX_TUNE
+// Tuning build only (tools/libgvx_tune.so): GVX_TMA_CFG / GVX_LDG_CFG pick
+// alternative tile / ring / occupancy variants of the f64 kernels.
+int tune_env(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+#endif
+
+// AoS pair kernels (mass, lab histogram, CM histogram) through the TMA ring.
+// Returns GVX_ERR_UNSUPPORTED when the histogram does not fit beside the ring
+// in shared memory (the caller then uses the LDG kernel).
+template <typename T, int C, int MODE, typename CFG>
+gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, void* m_out,
+                               const HistParams& hp, unsigned long long* bins, const gvx_vec4_view* bo,
+                               cudaStream_t s) {
+  const int nbs = MODE == PM_MASS ? 0 : hp.nbins + 2;
+  const size_t sm = CFG::smem_bytes(nbs);
+  if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
+  auto k = k_pair_tma<T, C, MODE, CFG>;
+  const int block = 32 * (CFG::NCW + 1);
+  int per_sm = blocks_per_sm(k, block, sm);
+  if (per_sm < 1) return GVX_ERR_UNSUPPORTED;
+  const int64_t ntiles = n / CFG::TILE;
+  int64_t full = (int64_t)sm_count() * per_sm;
+  int grid = (int)(ntiles < 1 ? 1 : (ntiles < full ? ntiles : full));
+  View4o<T> bov = mk4o<T>(bo);
+  // Per-CTA uint32 counters: one launch covers at most grid * 2^31 events.
+  const int64_t chunk = MODE == PM_MASS ? n : ((int64_t)grid << 31);
+  for (int64_t off = 0; off < n; off += chunk) {
+    int64_t cn = n - off < chunk ? n - off : chunk;
+    View4o<T> bo2 = bov;
+    if (bo)
+      for (int c = 0; c < 4; ++c) bo2.c[c] += 2 * off * bo2.s;
+    k<<<grid, block, sm, s>>>((const T*)v1->c[0] + 4 * off, (const T*)v2->c[0] + 4 * off, cn,
+                              m_out ? (T*)m_out + off : nullptr, hp, bins, bo2, bo != nullptr);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+template <typename T, int C, int MODE>
+gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, void* m_out,
+                           const HistParams& hp, unsigned long long* bins, const gvx_vec4_view* bo, cudaStream_t s) {
+#ifdef GVX_TUNE
+  if constexpr (sizeof(T) == 8 && C == C_PTETAPHIM) {
+    switch (tune_env("GVX_TMA_CFG")) {
+      case 1: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 4, 8, 3>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 2: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 512, 2, 8, 3>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 3: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 3, 8, 4>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 4: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 512, 6, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 5: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 6, 8, 2>>(v1, v2, n, m_out, hp, bins, bo, s);
+      default: break;
+    }
+  }
+#endif
+  return launch_pair_tma_cfg<T, C, MODE, typename TmaCfgOf<T>::type>(v1, v2, n, m_out, hp, bins, bo, s);
+}
+
 // ---------------------------------------------------------------- mass ------
 template <typename T, int C, int L>
 gvx_status launch_mass(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, void* m, int64_t n, cudaStream_t s) {
   constexpr int U = (L == L_AOS && sizeof(T) == 8) ? 2 : 1;
   constexpr int G = Group<T, L>::G;
-  auto k = k_invariant_mass<T, C, L, U>;
+  // f64 AoS: 64-register cap (4 CTAs/SM) measured fastest (sweep ldg1/ldg2).
+  auto k = (sizeof(T) == 8 && L == L_AOS) ? k_invariant_mass<T, C, L, U, 4> : k_invariant_mass<T, C, L, U>;
+#ifdef GVX_TUNE
+  if constexpr (sizeof(T) == 8 && L == L_AOS && C == C_PTETAPHIM) {
+    int v = tune_env("GVX_LDG_CFG");
+    if (v == 1) k = k_invariant_mass<T, C, L, U, 4>;
+    if (v == 2) k = k_invariant_mass<T, C, L, 1, 4>;
+    if (v == 3) k = k_invariant_mass<T, C, L, 1, 1>;
+  }
+#endif
   int grid = grid_for(k, kBlock, 0, (int64_t)kBlock * U * G, n);
   k<<<grid, kBlock, 0, s>>>(mk4<T>(v1), mk4<T>(v2), (T*)m, n);
   cudaError_t e = cudaGetLastError();
@@ -122,6 +246,11 @@ gvx_status dispatch_mass(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, voi
   int L = (l1 == l2) ? l1 : L_GEN;
   if (L == L_AOS && !aligned(m, Group<T, L_AOS>::G * sizeof(T))) L = L_GEN;  // vector stores
   if (L == L_SOA && !aligned(m, Group<T, L_SOA>::G * sizeof(T))) L = L_GEN;
+  if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, PM_MASS>()) {
+    HistParams hp{};
+    gvx_status st = launch_pair_tma<T, C, PM_MASS>(v1, v2, n, m, hp, nullptr, nullptr, s);
+    if (st != GVX_ERR_UNSUPPORTED) return st;
+  }
   if (L == L_AOS) return launch_mass<T, C, L_AOS>(v1, v2, m, n, s);
   if (L == L_SOA) return launch_mass<T, C, L_SOA>(v1, v2, m, n, s);
   return launch_mass<T, C, L_GEN>(v1, v2, m, n, s);
@@ -164,10 +293,18 @@ gvx_status launch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64
   View4o<T> bov = mk4o<T>(bo);
   cudaError_t e;
   if (smem) {
-    auto k = k_mass_histogram<T, C, L, CM, true>;
+    // f64 AoS: 4 CTAs/SM for the lab histogram, 3 for the heavier CM path (sweep ldg1/ldg4).
+    auto k = (sizeof(T) == 8 && L == L_AOS) ? (CM ? k_mass_histogram<T, C, L, CM, true, 3>
+                                                  : k_mass_histogram<T, C, L, CM, true, 4>)
+                                            : k_mass_histogram<T, C, L, CM, true>;
+#ifdef GVX_TUNE
+    if constexpr (sizeof(T) == 8 && L == L_AOS && C == C_PTETAPHIM) {
+      int v = tune_env("GVX_LDG_CFG");
+      if (v == 1 || v == 2) k = k_mass_histogram<T, C, L, CM, true, 4>;
+      if (v == 4) k = k_mass_histogram<T, C, L, CM, true, 3>;
+    }
+#endif
     size_t sm = nb2 * sizeof(unsigned int);
-    if (sm > 48 * 1024 && (e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
-      return cuda_fail(e);
     int grid = grid_for(k, kBlock, sm, (int64_t)kBlock * G, n);
     // Per-CTA uint32 counters: one launch covers at most grid * 2^31 events.
     const int64_t chunk = (int64_t)grid << 31;
@@ -199,6 +336,10 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
   int L = (l1 == l2) ? l1 : L_GEN;
   if (m_out && L == L_AOS && !aligned(m_out, Group<T, L_AOS>::G * sizeof(T))) L = L_GEN;
   if (m_out && L == L_SOA && !aligned(m_out, Group<T, L_SOA>::G * sizeof(T))) L = L_GEN;
+  if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, CM ? PM_HIST_CM : PM_HIST>()) {
+    gvx_status st = launch_pair_tma<T, C, CM ? PM_HIST_CM : PM_HIST>(v1, v2, n, m_out, hp, bins, bo, s);
+    if (st != GVX_ERR_UNSUPPORTED) return st;
+  }
   if (L == L_AOS) return launch_hist<T, C, L_AOS, CM>(v1, v2, n, hp, bins, m_out, bo, s);
   if (L == L_SOA) return launch_hist<T, C, L_SOA, CM>(v1, v2, n, hp, bins, m_out, bo, s);
   return launch_hist<T, C, L_GEN, CM>(v1, v2, n, hp, bins, m_out, bo, s);
@@ -279,7 +420,7 @@ gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4
   if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !bins || !aligned(bins, 8)) return GVX_ERR_INVALID_ARGUMENT;
   if (m_out && !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
   if (boosted_out && !out_view_ok(boosted_out, es)) return GVX_ERR_INVALID_ARGUMENT;
-  HistParams hp{lo, hi, hi - lo, nbins};
+  HistParams hp{lo, hi, hi - lo, 1.0 / (hi - lo), (double)nbins, nbins};
   cudaStream_t s = (cudaStream_t)stream;
 #define GVX_HIST_DISPATCH(T, C)                                                                                  \
   (cm ? dispatch_hist<T, C, true>(v1, v2, n, hp, bins, m_out, boosted_out, s)                       \

@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "gvx_math.cuh"
+#include "gvx_tma.cuh"
 
 namespace gvx {
 
@@ -111,8 +112,8 @@ __device__ __forceinline__ V4<T> to_cartesian(const T (&a)[4]) {
 // ============================================================================
 // K1: invariant mass
 // ============================================================================
-template <typename T, int COORDS, int L, int U>
-__global__ void __launch_bounds__(256) k_invariant_mass(View4<T> v1, View4<T> v2, T* __restrict__ m, int64_t n) {
+template <typename T, int COORDS, int L, int U, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_invariant_mass(View4<T> v1, View4<T> v2, T* __restrict__ m, int64_t n) {
   constexpr int G = Group<T, L>::G;
   const int64_t ngroups = n / G;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
@@ -197,11 +198,6 @@ __global__ void __launch_bounds__(256) k_boost(View4<T> v, View3<T> beta, View4o
 // ============================================================================
 // K3: fused mass (lab or CM frame) + histogram, privatised in shared memory.
 // ============================================================================
-struct HistParams {
-  double lo, hi, width;  // width = hi - lo (same IEEE value the oracle forms)
-  int nbins;
-};
-
 template <typename T, int COORDS, bool CM>
 __device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], int64_t i, const View4o<T>& bo,
                                              bool want_boosted) {
@@ -220,8 +216,8 @@ __device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], i
   }
 }
 
-template <typename T, int COORDS, int L, bool CM, bool SMEM>
-__global__ void __launch_bounds__(256) k_mass_histogram(View4<T> v1, View4<T> v2, int64_t n, HistParams hp,
+template <typename T, int COORDS, int L, bool CM, bool SMEM, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4<T> v2, int64_t n, HistParams hp,
                                                         unsigned long long* __restrict__ bins, T* __restrict__ m_out,
                                                         View4o<T> bo, bool want_boosted) {
   extern __shared__ unsigned int sh[];
@@ -232,7 +228,7 @@ __global__ void __launch_bounds__(256) k_mass_histogram(View4<T> v1, View4<T> v2
     __syncthreads();
   }
   auto count = [&](T M) {
-    int b = find_bin((double)M, hp.lo, hp.hi, hp.width, hp.nbins);
+    int b = find_bin((double)M, hp);
     if constexpr (SMEM) atomicAdd(&sh[b], 1u);
     else atomicAdd(&bins[b], 1ull);
   };
@@ -268,6 +264,139 @@ __global__ void __launch_bounds__(256) k_mass_histogram(View4<T> v1, View4<T> v2
     __syncthreads();
     for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
       unsigned int c = sh[b];
+      if (c) atomicAdd(&bins[b], (unsigned long long)c);
+    }
+  }
+}
+
+// ============================================================================
+// K1 / K3 on AoS pairs, TMA-fed (the fast path for the paper's LVector* layout).
+//
+// One CTA = 1 producer warp + NCW consumer warps, persistent over tiles of
+// TILE events (static round-robin). The producer's elected lane streams the
+// v1 and v2 tiles of each stage into a STAGES-deep shared-memory ring with
+// cp.async.bulk (UBLKCP, L2 evict-first) signalling a "full" mbarrier; the
+// consumers copy their events out of shared memory, release the stage on an
+// "empty" mbarrier (one arrive per warp) and only then do the arithmetic, so
+// HBM reads for later stages stay in flight while the FP64 pipe works —
+// bytes in flight are set by STAGES x TILE, not by register occupancy.
+// ============================================================================
+enum PairMode { PM_MASS = 0, PM_HIST = 1, PM_HIST_CM = 2 };
+
+template <typename T, int TILE_, int STAGES_, int NCW_, int MINB_ = 1>
+struct PairTma {
+  static constexpr int TILE = TILE_, STAGES = STAGES_, NCW = NCW_, MINB = MINB_;
+  static constexpr int NCT = NCW * 32;
+  static constexpr int EPT = TILE / NCT;
+  static constexpr int VEC = 4 * (int)sizeof(T);                 // bytes per 4-vector
+  static constexpr int HALF = TILE * VEC;                         // one array's tile
+  static constexpr int STAGE_BYTES = 2 * HALF;
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int BAR_BYTES = 2 * STAGES * 8;
+  static_assert(TILE % NCT == 0, "TILE must be a multiple of the consumer thread count");
+  static size_t smem_bytes(int nbins_smem) { return RING_BYTES + BAR_BYTES + (size_t)nbins_smem * 4; }
+};
+
+// Read event e's 4-vector from a stage buffer. fp64: two LDS.128 per vector
+// (lane stride 32 B: a 2-way bank conflict, cheaper here than the 16 FSELs a
+// swizzle costs in these issue-bound kernels).
+__device__ __forceinline__ void lds_vec(const double* base, int e, int, double (&x)[4]) {
+  const double2* p = reinterpret_cast<const double2*>(base + 4 * e);
+  double2 a = p[0], b = p[1];
+  x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+}
+__device__ __forceinline__ void lds_vec(const float* base, int e, int, float (&x)[4]) {
+  float4 a = *reinterpret_cast<const float4*>(base + 4 * e);
+  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+}
+
+template <typename T, int COORDS, int MODE>
+__device__ __forceinline__ void pair_consume(const T (&a)[4], const T (&b)[4], int64_t i, T* __restrict__ m_out,
+                                             unsigned int* sh_hist, const HistParams& hp, const View4o<T>& bo,
+                                             bool want_boosted) {
+  if constexpr (MODE == PM_MASS) {
+    m_out[i] = event_mass<T, COORDS>(a, b);
+  } else {
+    T M = hist_event_mass<T, COORDS, MODE == PM_HIST_CM>(a, b, i, bo, want_boosted);
+    atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+    if (m_out) m_out[i] = M;
+  }
+}
+
+template <typename T, int COORDS, int MODE, typename CFG>
+__global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(const T* __restrict__ v1, const T* __restrict__ v2,
+                                                                 int64_t n, T* __restrict__ m_out, HistParams hp,
+                                                                 unsigned long long* __restrict__ bins, View4o<T> bo,
+                                                                 bool want_boosted) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* ring = reinterpret_cast<T*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CFG::RING_BYTES);
+  uint64_t* empty = full + CFG::STAGES;
+  unsigned int* sh_hist = reinterpret_cast<unsigned int*>(smem + CFG::RING_BYTES + CFG::BAR_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb2 = hp.nbins + 2;
+
+  if constexpr (MODE != PM_MASS) {
+    for (int b = threadIdx.x; b < nb2; b += blockDim.x) sh_hist[b] = 0u;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CFG::STAGES; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], CFG::NCW);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+
+  const int64_t ntiles = n / CFG::TILE;
+  constexpr int TV = CFG::TILE * 4;  // scalars per array tile
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      const uint64_t pol = tma::policy_evict_first();
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it % CFG::STAGES, k = it / CFG::STAGES;
+        if (k > 0) tma::mbar_wait(&empty[s], (k - 1) & 1);
+        tma::mbar_arrive_expect_tx(&full[s], CFG::STAGE_BYTES);
+        T* dst = ring + (size_t)s * 2 * TV;
+        tma::bulk_g2s(dst, v1 + t * TV, CFG::HALF, &full[s], pol);
+        tma::bulk_g2s(dst + TV, v2 + t * TV, CFG::HALF, &full[s], pol);
+      }
+    }
+  } else {  // consumers
+    const int ctid = threadIdx.x - 32;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int s = it % CFG::STAGES, k = it / CFG::STAGES;
+      tma::mbar_wait(&full[s], k & 1);
+      const T* src = ring + (size_t)s * 2 * TV;
+      T a[CFG::EPT][4], b[CFG::EPT][4];
+#pragma unroll
+      for (int u = 0; u < CFG::EPT; ++u) {
+        lds_vec(src, u * CFG::NCT + ctid, lane, a[u]);
+        lds_vec(src + TV, u * CFG::NCT + ctid, lane, b[u]);
+      }
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[s]);
+#pragma unroll
+      for (int u = 0; u < CFG::EPT; ++u)
+        pair_consume<T, COORDS, MODE>(a[u], b[u], t * CFG::TILE + u * CFG::NCT + ctid, m_out, sh_hist, hp, bo,
+                                      want_boosted);
+    }
+    // ragged tail (< TILE events): the last CTA, plain loads
+    if (blockIdx.x == gridDim.x - 1) {
+      for (int64_t i = ntiles * CFG::TILE + ctid; i < n; i += CFG::NCT) {
+        T a[4], b[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { a[c] = v1[4 * i + c]; b[c] = v2[4 * i + c]; }
+        pair_consume<T, COORDS, MODE>(a, b, i, m_out, sh_hist, hp, bo, want_boosted);
+      }
+    }
+  }
+  if constexpr (MODE != PM_MASS) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
+      unsigned int c = sh_hist[b];
       if (c) atomicAdd(&bins[b], (unsigned long long)c);
     }
   }

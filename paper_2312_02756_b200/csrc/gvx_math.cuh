@@ -15,25 +15,194 @@
 //   where A+ = max(A, 0) (the E^2 clamp, R2) and t_i = E_i^2 - |p_i|^2
 //   = max(m_i|m_i|, -P_i). One cos, two exp, one sqrt of a product and one
 //   final sqrt replace two sincos, two sinh, three sqrt of the literal form.
-// Inputs outside the fast domain (|eta| > 20, huge |phi|, huge pt/m, NaN/Inf)
-// take the literal formula with IEEE-accurate libm (cold path).
+//
+// The fp64 transcendentals are B200-specific: the FP64 pipe (64 lanes/SM/clk,
+// measured 35.7 TFLOP/s) is the second roofline of the fp64 kernels, so
+// cos/sin/exp are short Taylor polynomials after a 2-FMA Cody-Waite reduction
+// (relative error <= ~2e-16 on the fast domain), sinh AND cosh come from ONE
+// even/odd split exp evaluation (e^r = E(r^2) + r O(r^2), e^-r = E - r O), and
+// reciprocals / square roots are MUFU.RCP64H / MUFU.RSQ64H seeds + Newton
+// (<= 2 ulp) instead of IEEE-exact division / sqrt. Inputs outside the fast
+// domain (|eta| > 20, |phi| > 1024, huge pt/m, NaN/Inf) take the literal
+// formula with IEEE-accurate libm (cold path, noinline).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace gvx {
 
+template <typename T> struct V4 { T x, y, z, t; };
+
+// ---------------------------------------------------------------------------
+// fp64 building blocks
+//
+// Polynomial coefficients live in __constant__ memory so every DFMA takes its
+// coefficient straight from the constant bank (c[0x3][...]) — 64-bit
+// immediates would otherwise cost two UMOVs per use and the fp64 kernels are
+// issue-bound as much as FP64-bound.
+// ---------------------------------------------------------------------------
+enum : int {
+  K_EXP_E = 0,    // 7 coefficients of E(s) = sum s^j/(2j)!, highest first (j = 6..0)
+  K_EXP_O = 7,    // 6 coefficients of O(s) = sum s^j/(2j+1)!, highest first (j = 5..0)
+  K_SIN = 13,     // 7 coefficients of (r - sin r)/r^3 series in z = r^2, highest first
+  K_COSQ = 20,    // 8 coefficients of (cos r - 1)/z series, highest first (for |r| <= pi/4)
+  K_COSH = 28,    // 11 coefficients of cos r = sum (-1)^j z^j/(2j)!, j = 10..0 (|r| <= pi/2)
+  K_LOG2E = 39, K_LN2_HI, K_LN2_LO, K_INV_PI, K_PI_HI, K_PI_LO, K_2_PI, K_PIO2_HI, K_PIO2_LO,
+  K_NCOEF
+};
+__constant__ double kCoef[K_NCOEF] = {
+    // E: 1/12!, 1/10!, 1/8!, 1/6!, 1/4!, 1/2!, 1
+    2.08767569878681e-09, 2.755731922398589e-07, 2.48015873015873e-05, 0.001388888888888889,
+    0.041666666666666664, 0.5, 1.0,
+    // O: 1/11!, 1/9!, 1/7!, 1/5!, 1/3!, 1
+    2.505210838544172e-08, 2.7557319223985893e-06, 0.0001984126984126984, 0.008333333333333333,
+    0.16666666666666666, 1.0,
+    // SIN: 1/15!, -1/13!, 1/11!, -1/9!, 1/7!, -1/5!, 1/3!   (sin r = r - r^3 * P(z))
+    7.647163731819816e-13, -1.6059043836821613e-10, 2.505210838544172e-08, -2.7557319223985893e-06,
+    0.0001984126984126984, -0.008333333333333333, 0.16666666666666666,
+    // COSQ: 1/16!, -1/14!, 1/12!, -1/10!, 1/8!, -1/6!, 1/4!, -1/2   (cos r = 1 + z * Q(z))
+    4.779477332387385e-14, -1.1470745597729725e-11, 2.08767569878681e-09, -2.755731922398589e-07,
+    2.48015873015873e-05, -0.001388888888888889, 0.041666666666666664, -0.5,
+    // COSH (cos on |r| <= pi/2, degree 20, truncation < 2e-17): (-1)^j/(2j)!, j = 10..0
+    4.110317623312165e-19, -1.5619206968586225e-16, 4.779477332387385e-14, -1.1470745597729725e-11,
+    2.08767569878681e-09, -2.755731922398589e-07, 2.48015873015873e-05, -0.001388888888888889,
+    0.041666666666666664, -0.5, 1.0,
+    // reduction constants
+    1.4426950408889634,       // log2(e)
+    6.93147180369123816490e-01, // LN2_HI = 0x3FE62E42FEE00000 (32 bits: k*LN2_HI exact)
+    1.90821492927058770002e-10, // LN2_LO = ln2 - LN2_HI
+    0.3183098861837907,       // 1/pi
+    3.141592653589793,        // PI_HI = double(pi)
+    1.2246467991473532e-16,   // PI_LO = pi - PI_HI
+    6.36619772367581382433e-01, // 2/pi
+    1.57079632679489655800e+00, // PIO2_HI = double(pi/2)
+    6.12323399573676603587e-17  // PIO2_LO = pi/2 - PIO2_HI
+};
+
+__device__ __forceinline__ double rcp_seed(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ double rsqrt_seed(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+// 1/x to <= 1 ulp for normal x (two Newton steps on the MUFU.RCP64H seed).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y = rcp_seed(x);
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+// 1/sqrt(x), x > 0 normal, <= 2 ulp (two Newton steps on MUFU.RSQ64H).
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y = rsqrt_seed(x);
+  double h = 0.5 * x;
+  double t = fma(-h, y * y, 0.5);
+  y = fma(y, t, y);
+  t = fma(-h, y * y, 0.5);
+  return fma(y, t, y);
+}
+// sqrt(x) for x >= 0 (x = 0 -> 0), <= 3 ulp: x * rsqrt(x).
+__device__ __forceinline__ double fast_sqrt(double x) {
+  double s = x * fast_rsqrt(x);
+  return x > 0.0 ? s : 0.0 * x;  // keeps +0, NaN propagates via 0*NaN
+}
+
+// Exact power of two 2^k for |k| < 1000 (integer ops only).
+__device__ __forceinline__ double pow2i(int k) { return __hiloint2double((k + 1023) << 20, 0); }
+
+// Round to nearest integer with the 1.5*2^52 shifter, valid for |v| < 2^51:
+// the integer lands in the low word of v + MAGIC. Replaces FRND.F64 and
+// F2I.F64, which run on the narrow XU pipe (ncu showed it oversubscribed).
+__device__ __forceinline__ double rint_shift(double v, int& ki) {
+  const double MAGIC = 6755399441055744.0;  // 1.5 * 2^52
+  double t = __dadd_rn(v, MAGIC);
+  ki = __double2loint(t);
+  return __dsub_rn(t, MAGIC);
+}
+
+// sinh and cosh of x, |x| <= 20: x = k ln2 + r, |r| <= ln2/2;
+// e^r = E + O, e^-r = E - O with E = sum r^2j/(2j)!, O = r sum r^2j/(2j+1)!
+// (Taylor to degree 12: truncation < 2e-16 relative).
+__device__ __forceinline__ void sinh_cosh(double x, double& sh, double& ch) {
+  int ki;
+  double k = rint_shift(x * kCoef[K_LOG2E], ki);
+  double r = fma(-k, kCoef[K_LN2_HI], x);
+  r = fma(-k, kCoef[K_LN2_LO], r);
+  double s = r * r;
+  double E = fma(s, kCoef[K_EXP_E + 0], kCoef[K_EXP_E + 1]);
+#pragma unroll
+  for (int j = 2; j < 7; ++j) E = fma(s, E, kCoef[K_EXP_E + j]);
+  double O = fma(s, kCoef[K_EXP_O + 0], kCoef[K_EXP_O + 1]);
+#pragma unroll
+  for (int j = 2; j < 6; ++j) O = fma(s, O, kCoef[K_EXP_O + j]);
+  O = O * r;
+  double up = pow2i(ki - 1), dn = pow2i(-ki - 1);  // 2^k / 2, 2^-k / 2
+  double ep = (E + O) * up, em = (E - O) * dn;
+  sh = ep - em;
+  ch = ep + em;
+}
+
+// sin and cos of r, |r| <= pi/4 (Taylor, degree 15 / 16: error < 5e-17).
+__device__ __forceinline__ void sincos_poly(double r, double& s, double& c) {
+  double z = r * r;
+  double ps = fma(z, kCoef[K_SIN + 0], kCoef[K_SIN + 1]);
+#pragma unroll
+  for (int j = 2; j < 7; ++j) ps = fma(z, ps, kCoef[K_SIN + j]);
+  s = fma(-r * z, ps, r);  // r - r^3 (1/3! - z/5! + ...)
+  double pc = fma(z, kCoef[K_COSQ + 0], kCoef[K_COSQ + 1]);
+#pragma unroll
+  for (int j = 2; j < 8; ++j) pc = fma(z, pc, kCoef[K_COSQ + j]);
+  c = fma(z, pc, 1.0);
+}
+
+// Flip the sign of x when bit 0 of q is set (integer op on the high word).
+__device__ __forceinline__ double neg_if(double x, int q) {
+  return __hiloint2double(__double2hiint(x) ^ ((q & 1) << 31), __double2loint(x));
+}
+
+// sin and cos of x, |x| <= 2048: x = k pi/2 + r, |r| <= pi/4 (+ulp).
+__device__ __forceinline__ void fast_sincos(double x, double& sn, double& cs) {
+  int q;
+  double k = rint_shift(x * kCoef[K_2_PI], q);
+  double r = fma(-k, kCoef[K_PIO2_HI], x);  // exact for |k| < 2^11
+  r = fma(-k, kCoef[K_PIO2_LO], r);
+  double s, c;
+  sincos_poly(r, s, c);
+  // sin x = [s, c, -s, -c][q & 3], cos x = [c, -s, -c, s][q & 3]
+  double ss = (q & 1) ? c : s;
+  double cc = (q & 1) ? s : c;
+  sn = neg_if(ss, q >> 1);
+  cs = neg_if(cc, (q + 1) >> 1);
+}
+
+// cos x, |x| <= 2048: x = k pi + r, |r| <= pi/2, cos x = (-1)^k cos r with a
+// degree-20 even polynomial — no quadrant selects.
+__device__ __forceinline__ double fast_cos(double x) {
+  int ki;
+  double k = rint_shift(x * kCoef[K_INV_PI], ki);
+  double r = fma(-k, kCoef[K_PI_HI], x);  // exact for |k| < 2^10
+  r = fma(-k, kCoef[K_PI_LO], r);
+  double z = r * r;
+  double c = fma(z, kCoef[K_COSH + 0], kCoef[K_COSH + 1]);
+#pragma unroll
+  for (int j = 2; j < 11; ++j) c = fma(z, c, kCoef[K_COSH + j]);
+  return neg_if(c, ki);
+}
+
 // ---------------------------------------------------------------------------
 // Literal conversion + sum + signed mass (cold path and PxPyPzE path).
 // ---------------------------------------------------------------------------
-template <typename T> struct V4 { T x, y, z, t; };
-
-__device__ __forceinline__ double d_sqrt(double x) { return sqrt(x); }
-__device__ __forceinline__ float d_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double ieee_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float ieee_sqrt(float x) { return sqrtf(x); }
 
 template <typename T>
 __device__ __forceinline__ T signed_sqrt(T m2) {
-  return m2 >= T(0) ? d_sqrt(m2) : -d_sqrt(-m2);
+  return m2 >= T(0) ? ieee_sqrt(m2) : -ieee_sqrt(-m2);
 }
 
 // PtEtaPhiM -> PxPyPzE with accurate libm (clamp R2).
@@ -67,35 +236,44 @@ __device__ __forceinline__ T mass_of_sum(const V4<T>& a, const V4<T>& b) {
 }
 
 template <typename T>
-__device__ __noinline__ T pair_mass_exact(T pt1, T eta1, T phi1, T m1, T pt2, T eta2, T phi2,
-                                          T m2) {
+__device__ __noinline__ T pair_mass_exact(T pt1, T eta1, T phi1, T m1, T pt2, T eta2, T phi2, T m2) {
   return mass_of_sum(ptetaphim_exact(pt1, eta1, phi1, m1), ptetaphim_exact(pt2, eta2, phi2, m2));
 }
 
 // ---------------------------------------------------------------------------
-// Fast fp64 pair mass (reduced form above).
+// Fast domain and fast pair mass.
 // ---------------------------------------------------------------------------
+// Fast domain, tested on the high words with integer compares (ALU pipe):
+// |eta| < 20, |phi| < 1024, |pt|, |m| < 2^200; NaN/Inf fail every test.
+__device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double2hiint(x) & 0x7fffffffu; }
 __device__ __forceinline__ bool fast_domain(double pt, double eta, double phi, double m) {
-  return fabs(eta) <= 20.0 && fabs(phi) <= 1024.0 && fabs(pt) <= 1e60 && fabs(m) <= 1e60;
+  return (abs_hi(eta) < 0x40340000u) & (abs_hi(phi) < 0x40900000u) & (abs_hi(pt) < 0x4C700000u) &
+         (abs_hi(m) < 0x4C700000u);
 }
+// f32: |eta| < 20, |phi| < 8, |pt|, |m| < 2^20.
+__device__ __forceinline__ uint32_t abs_bits(float x) { return (uint32_t)__float_as_int(x) & 0x7fffffffu; }
 __device__ __forceinline__ bool fast_domain(float pt, float eta, float phi, float m) {
-  return fabsf(eta) <= 20.f && fabsf(phi) <= 8.f && fabsf(pt) <= 1e6f && fabsf(m) <= 1e6f;
+  return (abs_bits(eta) < 0x41A00000u) & (abs_bits(phi) < 0x41000000u) & (abs_bits(pt) < 0x49800000u) &
+         (abs_bits(m) < 0x49800000u);
 }
 
-__device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double phi1, double m1,
-                                                 double pt2, double eta2, double phi2, double m2) {
-  double c = cos(phi1 - phi2);
-  double e1 = exp(eta1), e2 = exp(eta2);
-  double r1 = 1.0 / e1, r2 = 1.0 / e2;
-  double sh1 = 0.5 * (e1 - r1), ch1 = 0.5 * (e1 + r1);
-  double sh2 = 0.5 * (e2 - r2), ch2 = 0.5 * (e2 + r2);
+__device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double phi1, double m1, double pt2,
+                                                 double eta2, double phi2, double m2) {
+  double c = fast_cos(phi1 - phi2);
+  double sh1, ch1, sh2, ch2;
+  sinh_cosh(eta1, sh1, ch1);
+  sinh_cosh(eta2, sh2, ch2);
   double q1 = pt1 * ch1, q2 = pt2 * ch2;
   double P1 = q1 * q1, P2 = q2 * q2;
   double mm1 = m1 * fabs(m1), mm2 = m2 * fabs(m2);
-  double A1 = fmax(mm1 + P1, 0.0), A2 = fmax(mm2 + P2, 0.0);
-  double t = fmax(mm1, -P1) + fmax(mm2, -P2);
-  double m2sq = t + 2.0 * (sqrt(A1 * A2) - pt1 * pt2 * (c + sh1 * sh2));
-  return signed_sqrt(m2sq);
+  double A1 = mm1 + P1, A2 = mm2 + P2;
+  // E^2 clamp (R2): a clamped vector has E = 0 and E^2 - |p|^2 = -P.
+  bool c1 = A1 < 0.0, c2 = A2 < 0.0;
+  double t = (c1 ? -P1 : mm1) + (c2 ? -P2 : mm2);
+  double A12 = (c1 | c2) ? 0.0 : A1 * A2;
+  double m2sq = t + 2.0 * (fast_sqrt(A12) - pt1 * pt2 * (c + sh1 * sh2));
+  double r = fast_sqrt(fabs(m2sq));
+  return m2sq >= 0.0 ? r : -r;
 }
 
 // fp32: MUFU-based cos/exp/rcp/sqrt (error budget DESIGN.md §5: <= ~1e-6 E^2
@@ -118,15 +296,15 @@ __device__ __forceinline__ float fast_ex2(float x) {
 }
 __device__ __forceinline__ float reduce_2pi(float d) {
   const float INV_2PI = 0.159154943091895336f;
-  const float TWO_PI_HI = 6.28318548202514648f;    // float(2 pi)
-  const float TWO_PI_LO = -1.74845553146951715e-7f; // 2 pi - TWO_PI_HI
+  const float TWO_PI_HI = 6.28318548202514648f;     // float(2 pi)
+  const float TWO_PI_LO = -1.74845553146951715e-7f;  // 2 pi - TWO_PI_HI
   float k = rintf(d * INV_2PI);
   float r = fmaf(-k, TWO_PI_HI, d);
   return fmaf(-k, TWO_PI_LO, r);
 }
 
-__device__ __forceinline__ float pair_mass_fast(float pt1, float eta1, float phi1, float m1,
-                                                float pt2, float eta2, float phi2, float m2) {
+__device__ __forceinline__ float pair_mass_fast(float pt1, float eta1, float phi1, float m1, float pt2, float eta2,
+                                                float phi2, float m2) {
   const float LOG2E = 1.44269504088896341f;
   float c = __cosf(reduce_2pi(phi1 - phi2));
   float e1 = fast_ex2(eta1 * LOG2E), e2 = fast_ex2(eta2 * LOG2E);
@@ -143,8 +321,7 @@ __device__ __forceinline__ float pair_mass_fast(float pt1, float eta1, float phi
 }
 
 template <typename T>
-__device__ __forceinline__ T pair_mass_ptetaphim(T pt1, T eta1, T phi1, T m1, T pt2, T eta2,
-                                                 T phi2, T m2) {
+__device__ __forceinline__ T pair_mass_ptetaphim(T pt1, T eta1, T phi1, T m1, T pt2, T eta2, T phi2, T m2) {
   if (fast_domain(pt1, eta1, phi1, m1) && fast_domain(pt2, eta2, phi2, m2))
     return pair_mass_fast(pt1, eta1, phi1, m1, pt2, eta2, phi2, m2);
   return pair_mass_exact(pt1, eta1, phi1, m1, pt2, eta2, phi2, m2);
@@ -154,16 +331,15 @@ __device__ __forceinline__ T pair_mass_ptetaphim(T pt1, T eta1, T phi1, T m1, T 
 // PtEtaPhiM -> PxPyPzE, fast (for the CM path, which needs Cartesian vectors).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ V4<double> ptetaphim_fast(double pt, double eta, double phi, double m) {
-  double s, c;
-  sincos(phi, &s, &c);
-  double e = exp(eta), r = 1.0 / e;
-  double sh = 0.5 * (e - r), ch = 0.5 * (e + r);
+  double s, c, sh, ch;
+  fast_sincos(phi, s, c);
+  sinh_cosh(eta, sh, ch);
   double q = pt * ch;
   V4<double> o;
   o.x = pt * c;
   o.y = pt * s;
   o.z = pt * sh;
-  o.t = sqrt(fmax(m * fabs(m) + q * q, 0.0));
+  o.t = fast_sqrt(fmax(fma(m, fabs(m), q * q), 0.0));
   return o;
 }
 __device__ __forceinline__ V4<float> ptetaphim_fast(float pt, float eta, float phi, float m) {
@@ -192,21 +368,35 @@ __device__ __forceinline__ V4<T> ptetaphim_to_cartesian(T pt, T eta, T phi, T m)
 //   p' = p + (bg (beta.p) + gamma E) beta,   E' = gamma (E + beta.p)
 // which is Lambda * v written without forming Lambda. |beta| >= 1 -> NaN x 4.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double rsqrt_acc(double x) { return 1.0 / sqrt(x); }
-__device__ __forceinline__ float rsqrt_acc(float x) { return 1.0f / sqrtf(x); }
-
 template <typename T> struct BoostCoef { T bx, by, bz, g, bg; bool ok; };
 
+// Accurate (IEEE div/sqrt) coefficients: the standalone boost kernel is
+// HBM-bound with DP headroom, so it keeps correctly rounded gamma.
 template <typename T>
 __device__ __forceinline__ BoostCoef<T> boost_coef(T bx, T by, T bz) {
   BoostCoef<T> k;
   k.bx = bx; k.by = by; k.bz = bz;
   T b2 = bx * bx + by * by + bz * bz;
   k.ok = b2 < T(1);
-  T g = rsqrt_acc(T(1) - b2);
+  T g = T(1) / ieee_sqrt(T(1) - b2);
   k.g = g;
   k.bg = g * g / (T(1) + g);
   return k;
+}
+// Fast coefficients (MUFU seeds + Newton, <= 2 ulp) for the CM histogram,
+// whose fp64 variant is FP64-pipe bound.
+__device__ __forceinline__ BoostCoef<double> boost_coef_fast(double bx, double by, double bz) {
+  BoostCoef<double> k;
+  k.bx = bx; k.by = by; k.bz = bz;
+  double b2 = bx * bx + by * by + bz * bz;
+  k.ok = b2 < 1.0;
+  double g = fast_rsqrt(1.0 - b2);
+  k.g = g;
+  k.bg = g * g * fast_rcp(1.0 + g);
+  return k;
+}
+__device__ __forceinline__ BoostCoef<float> boost_coef_fast(float bx, float by, float bz) {
+  return boost_coef(bx, by, bz);
 }
 
 template <typename T>
@@ -226,13 +416,15 @@ __device__ __forceinline__ V4<T> apply_boost(const BoostCoef<T>& k, const V4<T>&
   return o;
 }
 
+__device__ __forceinline__ double any_rcp(double x) { return fast_rcp(x); }
+__device__ __forceinline__ float any_rcp(float x) { return 1.0f / x; }
+
 // CM-frame mass (reading R11): beta_cm = -P/E, boost both, sum, signed mass.
 template <typename T>
-__device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>* a_out,
-                                          V4<T>* b_out) {
+__device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>* a_out, V4<T>* b_out) {
   T Px = a.x + b.x, Py = a.y + b.y, Pz = a.z + b.z, E = a.t + b.t;
-  T inv = T(1) / E;
-  BoostCoef<T> k = boost_coef(-Px * inv, -Py * inv, -Pz * inv);
+  T inv = any_rcp(E);
+  BoostCoef<T> k = boost_coef_fast(-Px * inv, -Py * inv, -Pz * inv);
   k.ok = k.ok && (E > T(0));
   V4<T> a2 = apply_boost(k, a), b2 = apply_boost(k, b);
   if (a_out) { *a_out = a2; *b_out = b2; }
@@ -240,14 +432,31 @@ __device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>*
 }
 
 // ---------------------------------------------------------------------------
-// ROOT FindFixBin in double with IEEE-exact operations in the oracle's order
-// (reading R12): identical bins for identical mass bits.
+// ROOT FindFixBin in double, bit-identical to the oracle's
+//   1 + (int)((nbins * (x - lo)) / (hi - lo))
+// The quotient is first formed with a precomputed reciprocal (error a few
+// ulp); only when it lies within 1e-14 (relative) of an integer — where the
+// rounding of the exact IEEE division could change the truncation — is the
+// IEEE division evaluated, so the bin equals the oracle's for equal x.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int find_bin(double x, double lo, double hi, double width, int nbins) {
-  if (x < lo) return 0;
-  if (!(x < hi)) return nbins + 1;
-  double q = __ddiv_rn(__dmul_rn((double)nbins, __dsub_rn(x, lo)), width);
-  return 1 + __double2int_rz(q);
+struct HistParams {
+  double lo, hi, width, inv_width;  // width = hi - lo (same IEEE value the oracle forms)
+  double nbins_d;                   // (double)nbins
+  int nbins;
+};
+
+__device__ __forceinline__ int find_bin(double x, const HistParams& hp) {
+  if (x < hp.lo) return 0;
+  if (!(x < hp.hi)) return hp.nbins + 1;
+  double a = __dmul_rn(hp.nbins_d, __dsub_rn(x, hp.lo));
+  double q = a * hp.inv_width;
+  int qi;
+  double qr = rint_shift(q, qi);
+  if (fabs(q - qr) <= fmax(q, 1.0) * 1e-14) return 1 + __double2int_rz(__ddiv_rn(a, hp.width));
+  // q is not within 1e-14 of an integer: floor(q) = rint(q - 0.5) exactly
+  int fi;
+  rint_shift(q - 0.5, fi);
+  return 1 + fi;
 }
 
 }  // namespace gvx
