@@ -366,3 +366,18 @@ def test_cfg4_cfg5_histogram_1e9_f32(gvx, O, cm):
     inner = 1 + torch.trunc(torch.nan_to_num(q, nan=0.0, posinf=0.0, neginf=0.0)).long()
     b = torch.where(x < LO, 0, torch.where(~(x < HI), NB + 1, inner))
     assert torch.equal(torch.bincount(b, minlength=NB + 2), h)
+
+
+def test_tma_ring_kernels_all_modes():
+    """The TMA bulk-copy ring kernels are routed by default only where they measured faster
+    (f32 CM histogram); rerun the AoS parity tests with GVX_FORCE_TMA=1 so every mode and
+    dtype of the ring kernel is checked against the oracle too."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, GVX_FORCE_TMA="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", os.path.join(here, "test_gpu_parity.py"),
+                        "-k", "cfg1 or layouts or small_and_empty or histogram_parity or single_bin or nbins"],
+                       env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
