@@ -195,7 +195,7 @@ gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v
     if (bo)
       for (int c = 0; c < 4; ++c) bo2.c[c] += 2 * off * bo2.s;
     k<<<grid, block, sm, s>>>((const T*)v1->c[0] + 4 * off, (const T*)v2->c[0] + 4 * off, cn,
-                              m_out ? (T*)m_out + off : nullptr, hp, bins, bo2, bo != nullptr);
+                              m_out ? (T*)m_out + off : nullptr, hp, bins, bo2);
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GVX_OK : cuda_fail(e);
@@ -284,7 +284,9 @@ bool out_view_ok(const gvx_vec4_view* out, size_t es) { return view_ok<4>(out, e
 // ---------------------------------------------------------------- hist ------
 constexpr size_t kMaxSmemBins = 48 * 1024;  // uint32 bins in shared memory (192 KB)
 
-template <typename T, int C, int L, bool CM>
+// WBO: the CM kernel also writes the boosted pair (compile-time, so the
+// common path carries no output plumbing).
+template <typename T, int C, int L, bool CM, bool WBO = false>
 gvx_status launch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, const HistParams& hp,
                        unsigned long long* bins, void* m_out, const gvx_vec4_view* bo, cudaStream_t s) {
   constexpr int G = Group<T, L>::G;
@@ -294,11 +296,11 @@ gvx_status launch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64
   cudaError_t e;
   if (smem) {
     // f64 AoS: 4 CTAs/SM for the lab histogram, 3 for the heavier CM path (sweep ldg1/ldg4).
-    auto k = (sizeof(T) == 8 && L == L_AOS) ? (CM ? k_mass_histogram<T, C, L, CM, true, 3>
-                                                  : k_mass_histogram<T, C, L, CM, true, 4>)
-                                            : k_mass_histogram<T, C, L, CM, true>;
+    auto k = (sizeof(T) == 8 && L == L_AOS && !WBO) ? (CM ? k_mass_histogram<T, C, L, CM, true, 3>
+                                                          : k_mass_histogram<T, C, L, CM, true, 4>)
+                                                    : k_mass_histogram<T, C, L, CM, true, 1, WBO>;
 #ifdef GVX_TUNE
-    if constexpr (sizeof(T) == 8 && L == L_AOS && C == C_PTETAPHIM) {
+    if constexpr (sizeof(T) == 8 && L == L_AOS && C == C_PTETAPHIM && !WBO) {
       int v = tune_env("GVX_LDG_CFG");
       if (v == 1 || v == 2) k = k_mass_histogram<T, C, L, CM, true, 4>;
       if (v == 4) k = k_mass_histogram<T, C, L, CM, true, 3>;
@@ -318,12 +320,12 @@ gvx_status launch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64
         if (bo) bo2.c[c] += 2 * off * bo2.s;
       }
       T* mo = m_out ? (T*)m_out + off : nullptr;
-      k<<<grid, kBlock, sm, s>>>(a, b, cn, hp, bins, mo, bo2, bo != nullptr);
+      k<<<grid, kBlock, sm, s>>>(a, b, cn, hp, bins, mo, bo2);
     }
   } else {
-    auto k = k_mass_histogram<T, C, L, CM, false>;
+    auto k = k_mass_histogram<T, C, L, CM, false, 1, WBO>;
     int grid = grid_for(k, kBlock, 0, (int64_t)kBlock * G, n);
-    k<<<grid, kBlock, 0, s>>>(mk4<T>(v1), mk4<T>(v2), n, hp, bins, (T*)m_out, bov, bo != nullptr);
+    k<<<grid, kBlock, 0, s>>>(mk4<T>(v1), mk4<T>(v2), n, hp, bins, (T*)m_out, bov);
   }
   e = cudaGetLastError();
   return e == cudaSuccess ? GVX_OK : cuda_fail(e);
@@ -336,13 +338,20 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
   int L = (l1 == l2) ? l1 : L_GEN;
   if (m_out && L == L_AOS && !aligned(m_out, Group<T, L_AOS>::G * sizeof(T))) L = L_GEN;
   if (m_out && L == L_SOA && !aligned(m_out, Group<T, L_SOA>::G * sizeof(T))) L = L_GEN;
+  if constexpr (CM) {
+    if (bo) {  // boosted-pair output requested (diagnostic path)
+      if (L == L_AOS) return launch_hist<T, C, L_AOS, CM, true>(v1, v2, n, hp, bins, m_out, bo, s);
+      if (L == L_SOA) return launch_hist<T, C, L_SOA, CM, true>(v1, v2, n, hp, bins, m_out, bo, s);
+      return launch_hist<T, C, L_GEN, CM, true>(v1, v2, n, hp, bins, m_out, bo, s);
+    }
+  }
   if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, CM ? PM_HIST_CM : PM_HIST>()) {
-    gvx_status st = launch_pair_tma<T, C, CM ? PM_HIST_CM : PM_HIST>(v1, v2, n, m_out, hp, bins, bo, s);
+    gvx_status st = launch_pair_tma<T, C, CM ? PM_HIST_CM : PM_HIST>(v1, v2, n, m_out, hp, bins, nullptr, s);
     if (st != GVX_ERR_UNSUPPORTED) return st;
   }
-  if (L == L_AOS) return launch_hist<T, C, L_AOS, CM>(v1, v2, n, hp, bins, m_out, bo, s);
-  if (L == L_SOA) return launch_hist<T, C, L_SOA, CM>(v1, v2, n, hp, bins, m_out, bo, s);
-  return launch_hist<T, C, L_GEN, CM>(v1, v2, n, hp, bins, m_out, bo, s);
+  if (L == L_AOS) return launch_hist<T, C, L_AOS, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
+  if (L == L_SOA) return launch_hist<T, C, L_SOA, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
+  return launch_hist<T, C, L_GEN, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
 }
 
 }  // namespace

@@ -198,14 +198,20 @@ __global__ void __launch_bounds__(256) k_boost(View4<T> v, View3<T> beta, View4o
 // ============================================================================
 // K3: fused mass (lab or CM frame) + histogram, privatised in shared memory.
 // ============================================================================
-template <typename T, int COORDS, bool CM>
-__device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], int64_t i, const View4o<T>& bo,
-                                             bool want_boosted) {
+template <typename T, int COORDS, bool CM, bool WANT_BO = false>
+__device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], int64_t i, const View4o<T>& bo) {
   if constexpr (CM) {
-    V4<T> x = to_cartesian<T, COORDS>(a), y = to_cartesian<T, COORDS>(b);
     V4<T> xa, yb;
-    T M = cm_pair_mass(x, y, &xa, &yb);
-    if (want_boosted) {
+    T M;
+    if (COORDS == C_PTETAPHIM && fast_domain(a[0], a[1], a[2], a[3]) && fast_domain(b[0], b[1], b[2], b[3])) {
+      M = cm_mass_ptetaphim_fast(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3], WANT_BO ? &xa : nullptr, &yb);
+    } else if constexpr (COORDS == C_PTETAPHIM) {  // cold path: literal libm conversion
+      M = cm_pair_mass(ptetaphim_exact(a[0], a[1], a[2], a[3]), ptetaphim_exact(b[0], b[1], b[2], b[3]),
+                       WANT_BO ? &xa : nullptr, &yb);
+    } else {
+      M = cm_pair_mass(V4<T>{a[0], a[1], a[2], a[3]}, V4<T>{b[0], b[1], b[2], b[3]}, WANT_BO ? &xa : nullptr, &yb);
+    }
+    if constexpr (WANT_BO) {
       int64_t j0 = (2 * i) * bo.s, j1 = (2 * i + 1) * bo.s;
       bo.c[0][j0] = xa.x; bo.c[1][j0] = xa.y; bo.c[2][j0] = xa.z; bo.c[3][j0] = xa.t;
       bo.c[0][j1] = yb.x; bo.c[1][j1] = yb.y; bo.c[2][j1] = yb.z; bo.c[3][j1] = yb.t;
@@ -216,10 +222,10 @@ __device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], i
   }
 }
 
-template <typename T, int COORDS, int L, bool CM, bool SMEM, int MINB = 1>
+template <typename T, int COORDS, int L, bool CM, bool SMEM, int MINB = 1, bool WANT_BO = false>
 __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4<T> v2, int64_t n, HistParams hp,
                                                         unsigned long long* __restrict__ bins, T* __restrict__ m_out,
-                                                        View4o<T> bo, bool want_boosted) {
+                                                        View4o<T> bo) {
   extern __shared__ unsigned int sh[];
   constexpr int G = Group<T, L>::G;
   const int nb2 = hp.nbins + 2;
@@ -244,7 +250,7 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
     for (int j = 0; j < G; ++j) {
       T x[4] = {a[0][j], a[1][j], a[2][j], a[3][j]};
       T y[4] = {b[0][j], b[1][j], b[2][j], b[3][j]};
-      r[j] = hist_event_mass<T, COORDS, CM>(x, y, g * G + j, bo, want_boosted);
+      r[j] = hist_event_mass<T, COORDS, CM, WANT_BO>(x, y, g * G + j, bo);
       count(r[j]);
     }
     if (m_out) store_group<T, G>(m_out, g, r);
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
       T x[4], y[4];
       load_event(v1, i, x);
       load_event(v2, i, y);
-      T M = hist_event_mass<T, COORDS, CM>(x, y, i, bo, want_boosted);
+      T M = hist_event_mass<T, COORDS, CM, WANT_BO>(x, y, i, bo);
       count(M);
       if (m_out) m_out[i] = M;
     }
@@ -310,24 +316,22 @@ __device__ __forceinline__ void lds_vec(const float* base, int e, int, float (&x
   x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
 }
 
-template <typename T, int COORDS, int MODE>
+template <typename T, int COORDS, int MODE, bool WANT_BO>
 __device__ __forceinline__ void pair_consume(const T (&a)[4], const T (&b)[4], int64_t i, T* __restrict__ m_out,
-                                             unsigned int* sh_hist, const HistParams& hp, const View4o<T>& bo,
-                                             bool want_boosted) {
+                                             unsigned int* sh_hist, const HistParams& hp, const View4o<T>& bo) {
   if constexpr (MODE == PM_MASS) {
     m_out[i] = event_mass<T, COORDS>(a, b);
   } else {
-    T M = hist_event_mass<T, COORDS, MODE == PM_HIST_CM>(a, b, i, bo, want_boosted);
+    T M = hist_event_mass<T, COORDS, MODE == PM_HIST_CM, WANT_BO>(a, b, i, bo);
     atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
     if (m_out) m_out[i] = M;
   }
 }
 
-template <typename T, int COORDS, int MODE, typename CFG>
+template <typename T, int COORDS, int MODE, typename CFG, bool WANT_BO = false>
 __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(const T* __restrict__ v1, const T* __restrict__ v2,
                                                                  int64_t n, T* __restrict__ m_out, HistParams hp,
-                                                                 unsigned long long* __restrict__ bins, View4o<T> bo,
-                                                                 bool want_boosted) {
+                                                                 unsigned long long* __restrict__ bins, View4o<T> bo) {
   extern __shared__ __align__(128) unsigned char smem[];
   T* ring = reinterpret_cast<T*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CFG::RING_BYTES);
@@ -380,8 +384,8 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(con
       if (lane == 0) tma::mbar_arrive(&empty[s]);
 #pragma unroll
       for (int u = 0; u < CFG::EPT; ++u)
-        pair_consume<T, COORDS, MODE>(a[u], b[u], t * CFG::TILE + u * CFG::NCT + ctid, m_out, sh_hist, hp, bo,
-                                      want_boosted);
+        pair_consume<T, COORDS, MODE, WANT_BO>(a[u], b[u], t * CFG::TILE + u * CFG::NCT + ctid, m_out, sh_hist, hp,
+                                               bo);
     }
     // ragged tail (< TILE events): the last CTA, plain loads
     if (blockIdx.x == gridDim.x - 1) {
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(con
         T a[4], b[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) { a[c] = v1[4 * i + c]; b[c] = v2[4 * i + c]; }
-        pair_consume<T, COORDS, MODE>(a, b, i, m_out, sh_hist, hp, bo, want_boosted);
+        pair_consume<T, COORDS, MODE, WANT_BO>(a, b, i, m_out, sh_hist, hp, bo);
       }
     }
   }

@@ -18,7 +18,7 @@
 //
 // The fp64 transcendentals are B200-specific: the FP64 pipe (64 lanes/SM/clk,
 // measured 35.7 TFLOP/s) is the second roofline of the fp64 kernels, so
-// cos/sin/exp are short Taylor polynomials after a 2-FMA Cody-Waite reduction
+// cos/sin/exp are short near-minimax polynomials after a 2-FMA Cody-Waite reduction
 // (relative error <= ~2e-16 on the fast domain), sinh AND cosh come from ONE
 // even/odd split exp evaluation (e^r = E(r^2) + r O(r^2), e^-r = E - r O), and
 // reciprocals / square roots are MUFU.RCP64H / MUFU.RSQ64H seeds + Newton
@@ -42,41 +42,37 @@ template <typename T> struct V4 { T x, y, z, t; };
 // issue-bound as much as FP64-bound.
 // ---------------------------------------------------------------------------
 enum : int {
-  K_EXP_E = 0,    // 7 coefficients of E(s) = sum s^j/(2j)!, highest first (j = 6..0)
-  K_EXP_O = 7,    // 6 coefficients of O(s) = sum s^j/(2j+1)!, highest first (j = 5..0)
-  K_SIN = 13,     // 7 coefficients of (r - sin r)/r^3 series in z = r^2, highest first
-  K_COSQ = 20,    // 8 coefficients of (cos r - 1)/z series, highest first (for |r| <= pi/4)
-  K_COSH = 28,    // 11 coefficients of cos r = sum (-1)^j z^j/(2j)!, j = 10..0 (|r| <= pi/2)
-  K_LOG2E = 39, K_LN2_HI, K_LN2_LO, K_INV_PI, K_PI_HI, K_PI_LO, K_2_PI, K_PIO2_HI, K_PIO2_LO,
+  K_EXP_QE = 0,   // 4: cosh(r) = 1 + s(1/2 + s QE(s)), s = r^2, |r| <= ln2/2 (highest first)
+  K_EXP_QO = 4,   // 4: sinh(r)/r = 1 + s(1/6 + s QO(s))
+  K_SIN = 8,      // 6: sin r = r - r^3 P(z), z = r^2, |r| <= pi/4
+  K_COSQ = 14,    // 5: cos r = 1 + z(-1/2 + z Q(z)), |r| <= pi/4
+  K_COSH = 19,    // 9: cos r = C(z), |r| <= pi/2 (degree 16)
+  K_LOG2E = 28, K_LN2_HI, K_LN2_LO, K_INV_PI, K_PI_HI, K_PI_LO, K_2_PI, K_PIO2_HI, K_PIO2_LO,
   K_NCOEF
 };
+// Near-minimax coefficients (Chebyshev fits in 50-digit mpmath, rounded to
+// double). Max abs error with these doubles on the stated ranges:
+// cosh/sinh 2.2e-16 rel, sin 1.1e-16, cos(pi/4) 6.7e-16, cos(pi/2) 1.9e-16
+// (tests/test_fastmath_cpu.py re-derives these bounds from this table).
 __constant__ double kCoef[K_NCOEF] = {
-    // E: 1/12!, 1/10!, 1/8!, 1/6!, 1/4!, 1/2!, 1
-    2.08767569878681e-09, 2.755731922398589e-07, 2.48015873015873e-05, 0.001388888888888889,
-    0.041666666666666664, 0.5, 1.0,
-    // O: 1/11!, 1/9!, 1/7!, 1/5!, 1/3!, 1
-    2.505210838544172e-08, 2.7557319223985893e-06, 0.0001984126984126984, 0.008333333333333333,
-    0.16666666666666666, 1.0,
-    // SIN: 1/15!, -1/13!, 1/11!, -1/9!, 1/7!, -1/5!, 1/3!   (sin r = r - r^3 * P(z))
-    7.647163731819816e-13, -1.6059043836821613e-10, 2.505210838544172e-08, -2.7557319223985893e-06,
-    0.0001984126984126984, -0.008333333333333333, 0.16666666666666666,
-    // COSQ: 1/16!, -1/14!, 1/12!, -1/10!, 1/8!, -1/6!, 1/4!, -1/2   (cos r = 1 + z * Q(z))
-    4.779477332387385e-14, -1.1470745597729725e-11, 2.08767569878681e-09, -2.755731922398589e-07,
-    2.48015873015873e-05, -0.001388888888888889, 0.041666666666666664, -0.5,
-    // COSH (cos on |r| <= pi/2, degree 20, truncation < 2e-17): (-1)^j/(2j)!, j = 10..0
-    4.110317623312165e-19, -1.5619206968586225e-16, 4.779477332387385e-14, -1.1470745597729725e-11,
-    2.08767569878681e-09, -2.755731922398589e-07, 2.48015873015873e-05, -0.001388888888888889,
-    0.041666666666666664, -0.5, 1.0,
+    2.760751626492711e-07, 2.4801549607706326e-05, 0.0013888888897944966, 0.041666666666663264,      // QE
+    2.5090716821297755e-08, 2.755729023328528e-06, 0.00019841269848234848, 0.008333333333333071,    // QO
+    -1.5918129294866608e-10, 2.5051131845003624e-08, -2.755731610255244e-06, 0.00019841269836758574,
+    -0.008333333333330948, 0.16666666666666666,                                                     // SIN
+    2.0700600483433117e-09, -2.7556369695573007e-07, 2.4801585210990515e-05, -0.0013888888887277342,
+    0.04166666666666468,                                                                            // COSQ
+    4.608977003001797e-14, -1.1462901901757276e-11, 2.0876561839933163e-09, -2.755731639102575e-07,
+    2.4801587277414926e-05, -0.001388888888877299, 0.04166666666666388, -0.4999999999999997, 1.0,   // COSH
     // reduction constants
-    1.4426950408889634,       // log2(e)
-    6.93147180369123816490e-01, // LN2_HI = 0x3FE62E42FEE00000 (32 bits: k*LN2_HI exact)
-    1.90821492927058770002e-10, // LN2_LO = ln2 - LN2_HI
-    0.3183098861837907,       // 1/pi
-    3.141592653589793,        // PI_HI = double(pi)
-    1.2246467991473532e-16,   // PI_LO = pi - PI_HI
-    6.36619772367581382433e-01, // 2/pi
-    1.57079632679489655800e+00, // PIO2_HI = double(pi/2)
-    6.12323399573676603587e-17  // PIO2_LO = pi/2 - PIO2_HI
+    1.4426950408889634,          // log2(e)
+    6.93147180369123816490e-01,  // LN2_HI = 0x3FE62E42FEE00000 (32 bits: k*LN2_HI exact)
+    1.90821492927058770002e-10,  // LN2_LO = ln2 - LN2_HI
+    0.3183098861837907,          // 1/pi
+    3.141592653589793,           // PI_HI = double(pi)
+    1.2246467991473532e-16,      // PI_LO = pi - PI_HI
+    6.36619772367581382433e-01,  // 2/pi
+    1.57079632679489655800e+00,  // PIO2_HI = double(pi/2)
+    6.12323399573676603587e-17   // PIO2_LO = pi/2 - PIO2_HI
 };
 
 __device__ __forceinline__ double rcp_seed(double x) {
@@ -115,6 +111,12 @@ __device__ __forceinline__ double fast_sqrt(double x) {
 // Exact power of two 2^k for |k| < 1000 (integer ops only).
 __device__ __forceinline__ double pow2i(int k) { return __hiloint2double((k + 1023) << 20, 0); }
 
+// x * 2^k for normal x and a result that stays normal (integer add on the
+// exponent field of the high word).
+__device__ __forceinline__ double add_exponent(double x, int k) {
+  return __hiloint2double(__double2hiint(x) + (k << 20), __double2loint(x));
+}
+
 // Round to nearest integer with the 1.5*2^52 shifter, valid for |v| < 2^51:
 // the integer lands in the low word of v + MAGIC. Replaces FRND.F64 and
 // F2I.F64, which run on the narrow XU pipe (ncu showed it oversubscribed).
@@ -127,37 +129,39 @@ __device__ __forceinline__ double rint_shift(double v, int& ki) {
 
 // sinh and cosh of x, |x| <= 20: x = k ln2 + r, |r| <= ln2/2;
 // e^r = E + O, e^-r = E - O with E = sum r^2j/(2j)!, O = r sum r^2j/(2j+1)!
-// (Taylor to degree 12: truncation < 2e-16 relative).
+// (near-minimax degree 10 / 11: error <= 2.2e-16 relative).
 __device__ __forceinline__ void sinh_cosh(double x, double& sh, double& ch) {
   int ki;
   double k = rint_shift(x * kCoef[K_LOG2E], ki);
   double r = fma(-k, kCoef[K_LN2_HI], x);
   r = fma(-k, kCoef[K_LN2_LO], r);
   double s = r * r;
-  double E = fma(s, kCoef[K_EXP_E + 0], kCoef[K_EXP_E + 1]);
-#pragma unroll
-  for (int j = 2; j < 7; ++j) E = fma(s, E, kCoef[K_EXP_E + j]);
-  double O = fma(s, kCoef[K_EXP_O + 0], kCoef[K_EXP_O + 1]);
-#pragma unroll
-  for (int j = 2; j < 6; ++j) O = fma(s, O, kCoef[K_EXP_O + j]);
-  O = O * r;
-  double up = pow2i(ki - 1), dn = pow2i(-ki - 1);  // 2^k / 2, 2^-k / 2
-  double ep = (E + O) * up, em = (E - O) * dn;
+  double qe = fma(s, kCoef[K_EXP_QE + 0], kCoef[K_EXP_QE + 1]);
+  qe = fma(s, qe, kCoef[K_EXP_QE + 2]);
+  qe = fma(s, qe, kCoef[K_EXP_QE + 3]);
+  double E = fma(s, fma(s, qe, 0.5), 1.0);
+  double qo = fma(s, kCoef[K_EXP_QO + 0], kCoef[K_EXP_QO + 1]);
+  qo = fma(s, qo, kCoef[K_EXP_QO + 2]);
+  qo = fma(s, qo, kCoef[K_EXP_QO + 3]);
+  double O = fma(s, fma(s, qo, 0.16666666666666666), 1.0) * r;
+  // (E +- O) * 2^(+-k-1) by adding to the exponent field (exact: E +- O is in
+  // [0.7, 1.5], |k| <= 29) — an integer add instead of building 2^k and a DMUL.
+  double ep = add_exponent(E + O, ki - 1), em = add_exponent(E - O, -ki - 1);
   sh = ep - em;
   ch = ep + em;
 }
 
-// sin and cos of r, |r| <= pi/4 (Taylor, degree 15 / 16: error < 5e-17).
+// sin and cos of r, |r| <= pi/4 (near-minimax, degree 13 / 12).
 __device__ __forceinline__ void sincos_poly(double r, double& s, double& c) {
   double z = r * r;
   double ps = fma(z, kCoef[K_SIN + 0], kCoef[K_SIN + 1]);
 #pragma unroll
-  for (int j = 2; j < 7; ++j) ps = fma(z, ps, kCoef[K_SIN + j]);
-  s = fma(-r * z, ps, r);  // r - r^3 (1/3! - z/5! + ...)
+  for (int j = 2; j < 6; ++j) ps = fma(z, ps, kCoef[K_SIN + j]);
+  s = fma(-r * z, ps, r);  // r - r^3 P(z)
   double pc = fma(z, kCoef[K_COSQ + 0], kCoef[K_COSQ + 1]);
 #pragma unroll
-  for (int j = 2; j < 8; ++j) pc = fma(z, pc, kCoef[K_COSQ + j]);
-  c = fma(z, pc, 1.0);
+  for (int j = 2; j < 5; ++j) pc = fma(z, pc, kCoef[K_COSQ + j]);
+  c = fma(z, fma(z, pc, -0.5), 1.0);
 }
 
 // Flip the sign of x when bit 0 of q is set (integer op on the high word).
@@ -181,7 +185,7 @@ __device__ __forceinline__ void fast_sincos(double x, double& sn, double& cs) {
 }
 
 // cos x, |x| <= 2048: x = k pi + r, |r| <= pi/2, cos x = (-1)^k cos r with a
-// degree-20 even polynomial — no quadrant selects.
+// degree-16 even near-minimax polynomial — no quadrant selects.
 __device__ __forceinline__ double fast_cos(double x) {
   int ki;
   double k = rint_shift(x * kCoef[K_INV_PI], ki);
@@ -190,7 +194,7 @@ __device__ __forceinline__ double fast_cos(double x) {
   double z = r * r;
   double c = fma(z, kCoef[K_COSH + 0], kCoef[K_COSH + 1]);
 #pragma unroll
-  for (int j = 2; j < 11; ++j) c = fma(z, c, kCoef[K_COSH + j]);
+  for (int j = 2; j < 9; ++j) c = fma(z, c, kCoef[K_COSH + j]);
   return neg_if(c, ki);
 }
 
@@ -396,7 +400,15 @@ __device__ __forceinline__ BoostCoef<double> boost_coef_fast(double bx, double b
   return k;
 }
 __device__ __forceinline__ BoostCoef<float> boost_coef_fast(float bx, float by, float bz) {
-  return boost_coef(bx, by, bz);
+  BoostCoef<float> k;
+  k.bx = bx; k.by = by; k.bz = bz;
+  float b2 = bx * bx + by * by + bz * bz;
+  k.ok = b2 < 1.0f;
+  float g;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(1.0f - b2));
+  k.g = g;
+  k.bg = g * g * fast_rcp(1.0f + g);
+  return k;
 }
 
 template <typename T>
@@ -417,18 +429,76 @@ __device__ __forceinline__ V4<T> apply_boost(const BoostCoef<T>& k, const V4<T>&
 }
 
 __device__ __forceinline__ double any_rcp(double x) { return fast_rcp(x); }
-__device__ __forceinline__ float any_rcp(float x) { return 1.0f / x; }
+__device__ __forceinline__ float any_rcp(float x) { return fast_rcp(x); }
+
+// Signed square root with the fast sqrt (fp64: MUFU.RSQ64H + Newton, <= 3 ulp).
+__device__ __forceinline__ double fast_signed_sqrt(double m2) {
+  double r = fast_sqrt(fabs(m2));
+  return m2 >= 0.0 ? r : -r;
+}
+__device__ __forceinline__ float fast_signed_sqrt(float m2) {
+  float r = fast_sqrt(fabsf(m2));
+  return m2 >= 0.f ? r : -r;
+}
 
 // CM-frame mass (reading R11): beta_cm = -P/E, boost both, sum, signed mass.
+// E <= 0 or beta^2 >= 1 (or NaN) -> gamma = NaN, so every output is NaN
+// without a branch.
 template <typename T>
 __device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>* a_out, V4<T>* b_out) {
   T Px = a.x + b.x, Py = a.y + b.y, Pz = a.z + b.z, E = a.t + b.t;
   T inv = any_rcp(E);
   BoostCoef<T> k = boost_coef_fast(-Px * inv, -Py * inv, -Pz * inv);
-  k.ok = k.ok && (E > T(0));
+  const bool ok = k.ok && (E > T(0));
+  k.g = ok ? k.g : T(NAN);
+  k.bg = ok ? k.bg : T(NAN);
+  k.ok = true;
   V4<T> a2 = apply_boost(k, a), b2 = apply_boost(k, b);
   if (a_out) { *a_out = a2; *b_out = b2; }
-  return mass_of_sum(a2, b2);
+  T X = a2.x + b2.x, Y = a2.y + b2.y, Z = a2.z + b2.z, W = a2.t + b2.t;
+  return fast_signed_sqrt(W * W - (X * X + Y * Y + Z * Z));
+}
+
+// fp32 sincos / sinh+cosh with the same interface as the fp64 routines.
+__device__ __forceinline__ void fast_sincos(float x, float& sn, float& cs) { __sincosf(reduce_2pi(x), &sn, &cs); }
+__device__ __forceinline__ void sinh_cosh(float x, float& sh, float& ch) {
+  const float LOG2E = 1.44269504088896341f;
+  float e = fast_ex2(x * LOG2E), r = fast_rcp(e);
+  sh = 0.5f * (e - r);
+  ch = 0.5f * (e + r);
+}
+__device__ __forceinline__ double pos_sqrt(double x) { return fast_sqrt(x > 0.0 ? x : 0.0); }
+__device__ __forceinline__ float pos_sqrt(float x) { return fast_sqrt(x > 0.f ? x : 0.f); }
+
+// CM-frame mass of a PtEtaPhiM pair (fast domain), computed in coordinates
+// rotated about the z axis by -phi1. A rotation about z is a change of
+// Cartesian axes: the CM boost is still built from beta_cm = -P/E and applied
+// to both vectors literally, but vector 1 becomes (pt1, 0, pt1 sinh eta1, E1)
+// and vector 2 needs only sin/cos of phi2 - phi1 — one sincos per pair instead
+// of two. Boosted vectors, when requested, are rotated back by +phi1.
+template <typename T>
+__device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1, T pt2, T eta2, T phi2, T m2,
+                                                    V4<T>* a_out, V4<T>* b_out) {
+  T sd, cd, sh1, ch1, sh2, ch2;
+  fast_sincos(phi2 - phi1, sd, cd);
+  sinh_cosh(eta1, sh1, ch1);
+  sinh_cosh(eta2, sh2, ch2);
+  T q1 = pt1 * ch1, q2 = pt2 * ch2;
+  V4<T> a{pt1, T(0), pt1 * sh1, pos_sqrt(m1 * (m1 < T(0) ? -m1 : m1) + q1 * q1)};
+  V4<T> b{pt2 * cd, pt2 * sd, pt2 * sh2, pos_sqrt(m2 * (m2 < T(0) ? -m2 : m2) + q2 * q2)};
+  T M = cm_pair_mass(a, b, a_out, b_out);
+  if (a_out) {
+    T s1, c1;
+    fast_sincos(phi1, s1, c1);
+    V4<T>* v[2] = {a_out, b_out};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      T x = v[i]->x, y = v[i]->y;
+      v[i]->x = c1 * x - s1 * y;
+      v[i]->y = s1 * x + c1 * y;
+    }
+  }
+  return M;
 }
 
 // ---------------------------------------------------------------------------
@@ -452,11 +522,9 @@ __device__ __forceinline__ int find_bin(double x, const HistParams& hp) {
   double q = a * hp.inv_width;
   int qi;
   double qr = rint_shift(q, qi);
-  if (fabs(q - qr) <= fmax(q, 1.0) * 1e-14) return 1 + __double2int_rz(__ddiv_rn(a, hp.width));
-  // q is not within 1e-14 of an integer: floor(q) = rint(q - 0.5) exactly
-  int fi;
-  rint_shift(q - 0.5, fi);
-  return 1 + fi;
+  if (fabs(q - qr) <= q * 1e-14 + 1e-300) return 1 + __double2int_rz(__ddiv_rn(a, hp.width));
+  // q is not within 1e-14 of an integer, so floor(q) = floor(a / width)
+  return 1 + qi - (qr > q ? 1 : 0);
 }
 
 }  // namespace gvx
