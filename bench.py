@@ -46,11 +46,12 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--dtype", choices=["f64", "f32"], default="f64")
-    p.add_argument("--n", type=float, default=1e8, help="events per GPU")
+    p.add_argument("--events", type=float, default=1e8, help="events per GPU")
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=1 << 22, help="events in the oracle's bounded sample")
+    p.add_argument("--dist-backend", default="nccl", help="process-group backend for N>1 (nccl on B200s)")
     return p.parse_args()
 
 
@@ -138,7 +139,7 @@ def run_reference(args):
 
 
 def config_obj(args, world, ref_sample=None):
-    n = int(args.n)
+    n = int(args.events)
     es = 8 if args.dtype == "f64" else 4
     in_bytes = n * (8 * es + 7 * es)
     c = {"workload": f"GenVectorX hot path step: mass + per-event boost + lab & CM 1000-bin histograms, "
@@ -146,7 +147,7 @@ def config_obj(args, world, ref_sample=None):
          "n_events_per_gpu": n, "global_events": n * world, "layout": "AoS",
          "hist": {"lo": LO, "hi": HI, "nbins": NB},
          "l2": f"inputs larger than L2 ({in_bytes / 1e9:.1f} GB per GPU >> 126 MB), no flush needed",
-         "parallelism": f"dp{world} (event-index shards, NCCL bin all-reduce)"}
+         "parallelism": f"dp{world} (event-index shards, {getattr(args, 'dist_backend', 'nccl')} bin all-reduce)"}
     if ref_sample:
         c["reference_sample_events"] = ref_sample
     return c
@@ -226,11 +227,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # GVX_BENCH_SAME_DEVICE=1 maps every rank to cuda:0 — only for exercising the
+    # multi-rank code path on a one-GPU box (with --dist-backend gloo); never for numbers.
+    if os.environ.get("GVX_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    n = int(args.n)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
+    n = int(args.events)
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
     es = 8 if args.dtype == "f64" else 4
     first = rank * n  # this rank's shard of the global event index space
@@ -309,7 +317,7 @@ def run_ours(args):
                       "achieved_GBs": gbs, "frac_of_peak": gbs / peak}
     dom = max(KERNEL_ORDER, key=lambda k: kernels[k]["ms"])
     roofline = {"bound": "hbm", "kernel": f"gvx_{dom}", "achieved": kernels[dom]["achieved_GBs"], "peak": peak,
-                "unit": "GB/s", "frac": kernels[dom]["frac_of_peak"], "traffic": ncu_traffic(dom, args.dtype),
+                "unit": "GB/s", "frac": kernels[dom]["frac_of_peak"], "traffic": ncu_traffic(dom, args.dtype, n),
                 "peak_source": peak_kind,
                 "bytes_per_launch": n * BYTES[dom](es)}
 
@@ -337,14 +345,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def ncu_traffic(kernel: str, dtype: str):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
-    summary (profiles/ncu_traffic.json, written by tools/ncu_summary.py), else None."""
+def ncu_traffic(kernel: str, dtype: str, n: int):
+    """DRAM bytes per launch of the dominant kernel, from the committed ncu --set full
+    capture summary (profiles/ncu_traffic.json, written by tools/ncu_summary.py): the
+    captured bytes per event times this launch's events, else None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d[dtype][kernel]["dram_bytes_per_launch"]
+            d = json.load(f)[dtype][kernel]
+        return d["dram_bytes_per_event"] * n
     except Exception:
         return None
 

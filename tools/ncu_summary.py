@@ -83,7 +83,8 @@ def main():
         dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
         ab = algo.get(key, 0) * n
         lines.append(f"| `{key}` ({name[:60]}) | " + " | ".join(vals) + f" | {ab:.3e} | {dram / ab if ab else 0:.3f} |")
-        traffic[key] = {"dram_bytes_per_launch": dram, "algorithmic_bytes_per_launch": ab, "kernel": name[:120]}
+        traffic[key] = {"dram_bytes_per_launch": dram, "algorithmic_bytes_per_launch": ab, "events_per_launch": n,
+                        "dram_bytes_per_event": dram / n, "kernel": name[:120]}
     os.makedirs(rdir, exist_ok=True)
     with open(os.path.join(rdir, f"ncu_summary_{dtype}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")

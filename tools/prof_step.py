@@ -14,12 +14,12 @@ import synth.device as sd  # noqa: E402
 
 p = argparse.ArgumentParser()
 p.add_argument("--dtype", default="f64")
-p.add_argument("--n", type=float, default=1e8)
+p.add_argument("--events", type=float, default=1e8)
 p.add_argument("--reps", type=int, default=1)
 p.add_argument("--layout", default="aos")
 a = p.parse_args()
 tdt = torch.float64 if a.dtype == "f64" else torch.float32
-n = int(a.n)
+n = int(a.events)
 v1, v2 = sd.muon_pairs(n, dtype=tdt)
 bv, bb = sd.boost_inputs(n, dtype=tdt)
 if a.layout == "soa":
