@@ -142,23 +142,31 @@ bool tma_enabled() {
 }
 
 // Which AoS pair kernels take the TMA ring by default. Measured on B200
-// (profiles/r01/sweep_f64_variants.jsonl, bench_{tma,ldg}_*.jsonl): the ring
-// wins only for the f32 CM histogram; the f64 kernels are FP64/issue-bound and
-// do better with the register-resident LDG kernels at higher occupancy.
-// GVX_FORCE_TMA=1 routes every AoS pair kernel through the ring.
+// (profiles/r01/sweep_f64_variants*.jsonl): every fp64 pair kernel (the
+// ring frees the registers the LDG kernels spend on loads in flight, so one
+// CTA of 29-32 warps keeps the FP64 pipe fed) and the fp32 histograms
+// (profiles/r01/sweep_f32_variants.jsonl); the fp32 mass kernel runs faster
+// from registers (LDG.256). GVX_FORCE_TMA=1 routes every AoS pair kernel
+// through the ring (tested).
 template <typename T, int MODE>
 bool tma_preferred() {
   static const bool force = [] {
     const char* e = getenv("GVX_FORCE_TMA");
     return e && e[0] == '1';
   }();
-  return force || (sizeof(T) == 4 && MODE == PM_HIST_CM);
+  return force || sizeof(T) == 8 || MODE != PM_MASS;
 }
 
 // ------------------------------------------------------- TMA pair stream ----
-template <typename T> struct TmaCfgOf;
-template <> struct TmaCfgOf<double> { using type = PairTma<double, 512, 3, 8>; };
-template <> struct TmaCfgOf<float> { using type = PairTma<float, 512, 4, 8>; };
+// Ring geometry per (dtype, mode), from the B200 sweeps in profiles/r01/
+// (sweep_f64_variants*.jsonl): one CTA per SM with 28-31 consumer warps and a
+// 2-3 stage ring of 57-62 KB stages beat 2-3 smaller CTAs, because the fp64
+// consumers need warps (FP64 latency) more than ring depth.
+template <typename T, int MODE> struct TmaCfgOf;
+template <int MODE> struct TmaCfgOf<double, MODE> { using type = PairTma<double, 896, 2, 28, 1>; };
+template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 992, 3, 31, 1>; };
+template <int MODE> struct TmaCfgOf<float, MODE> { using type = PairTma<float, 896, 4, 28, 1>; };
+template <> struct TmaCfgOf<float, PM_HIST_CM> { using type = PairTma<float, 1792, 3, 28, 1>; };
 
 #ifdef GVX_TUNE
 // Tuning build only (tools/libgvx_tune.so): GVX_TMA_CFG / GVX_LDG_CFG pick
@@ -212,11 +220,25 @@ gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, i
       case 3: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 3, 8, 4>>(v1, v2, n, m_out, hp, bins, bo, s);
       case 4: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 512, 6, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
       case 5: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 6, 8, 2>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 6: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 768, 4, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 7: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 640, 5, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 8: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 896, 3, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 9: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 992, 3, 31, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 10: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 448, 3, 14, 2>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 11: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 896, 2, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      default: break;
+    }
+  }
+  if constexpr (sizeof(T) == 4 && C == C_PTETAPHIM) {
+    switch (tune_env("GVX_TMA_CFG32")) {
+      case 1: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1792, 3, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 2: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 896, 4, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 3: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1024, 3, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
       default: break;
     }
   }
 #endif
-  return launch_pair_tma_cfg<T, C, MODE, typename TmaCfgOf<T>::type>(v1, v2, n, m_out, hp, bins, bo, s);
+  return launch_pair_tma_cfg<T, C, MODE, typename TmaCfgOf<T, MODE>::type>(v1, v2, n, m_out, hp, bins, bo, s);
 }
 
 // ---------------------------------------------------------------- mass ------
