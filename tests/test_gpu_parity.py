@@ -102,6 +102,8 @@ def test_cfg1_mass_65536_f64(gvx, O):
     assert bad.size == 0, (bad[:5], m[bad[:5]], mo[bad[:5]])
     rel = np.abs(m * np.abs(m) - mo * np.abs(mo)) / e ** 2
     print(f"cfg1 max |dM2|/E2 = {rel.max():.3e}")
+    # quality guard (not the parity bar): the fast f64 math is budgeted at ~1e-15 E^2
+    assert rel.max() <= 1e-13
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
@@ -381,3 +383,43 @@ def test_tma_ring_kernels_all_modes():
                         "-k", "cfg1 or layouts or small_and_empty or histogram_parity or single_bin or nbins"],
                        env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_hostpipe_matches_device_path(gvx):
+    """Transfer-inclusive mode (hostpipe) gives the same bits as the device-resident calls."""
+    import synth.device as sd
+    from paper_2312_02756_b200 import hostpipe
+    n = (1 << 20) + 12345
+    for tdt in (torch.float64, torch.float32):
+        v1, v2 = sd.muon_pairs(n, dtype=tdt)
+        bv, bb = sd.boost_inputs(n, dtype=tdt)
+        m = gvx.invariant_mass(v1, v2)
+        bo = gvx.boost(bv, bb)
+        h = gvx.mass_histogram(v1, v2)
+        hc = gvx.mass_histogram(v1, v2, cm=True)
+        hs = [t.cpu().pin_memory() for t in (v1, v2, bv, bb)]
+        pipe = hostpipe.HostPipeline(n, tdt, "cuda", chunk=1 << 18)
+        hm, hbo, hbins = pipe.step(*hs)
+        torch.cuda.synchronize()
+        assert torch.equal(hm, m.cpu()) and torch.equal(hbo, bo.cpu())
+        assert torch.equal(hbins[0], h.cpu()) and torch.equal(hbins[1], hc.cpu())
+
+
+def test_sharded_histogram_single_rank(gvx):
+    import synth.device as sd
+    v1, v2 = sd.muon_pairs(100_000, dtype=torch.float64)
+    assert torch.equal(gvx.sharded_mass_histogram(v1, v2), gvx.mass_histogram(v1, v2))
+
+
+def test_boosted_output_f32(gvx, O):
+    """CM boosted-pair output (diagnostic) in f32: checked at 1e-4·S for well-conditioned pairs
+    (DESIGN R5/R14: fp32 CM boosts of near-collinear pairs are ill-conditioned)."""
+    v1, v2 = synth.muon_pairs(np.arange(50_000), seed=3, dtype=np.float32)
+    _, _, bref = O.cm_mass(v1, v2, want_boosted=True)
+    mlab, e = O.invariant_mass(v1, v2)
+    bo = torch.empty((2 * v1.shape[0], 4), dtype=torch.float32, device="cuda")
+    gvx.mass_histogram(dev(v1), dev(v2), cm=True, boosted_out=bo)
+    bg = host(bo).reshape(-1, 8).astype(np.float64)
+    ok = np.isfinite(bref).all(1) & (np.abs(mlab) >= 1e-2 * e)
+    S = (e[ok].astype(np.float64) ** 2) / np.abs(mlab[ok].astype(np.float64))
+    assert (np.abs(bg[ok] - bref[ok]).max(1) / S).max() <= 1e-4
