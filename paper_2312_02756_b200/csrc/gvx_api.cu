@@ -45,6 +45,10 @@ int sm_count() {
 // memory limit the first time a size above 48 KB is requested.
 std::mutex g_occ_mu;
 std::map<std::tuple<const void*, int, size_t, int>, int> g_occ;
+// Largest dynamic shared memory opted in per (kernel, device): the attribute
+// is only ever raised, so a later call with fewer bins cannot invalidate a
+// cached launch configuration that needs more.
+std::map<std::pair<const void*, int>, size_t> g_smem_optin;
 
 template <typename K>
 int blocks_per_sm(K kernel, int block, size_t smem) {
@@ -55,8 +59,14 @@ int blocks_per_sm(K kernel, int block, size_t smem) {
     std::lock_guard<std::mutex> lk(g_occ_mu);
     auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
+    if (smem > 48 * 1024) {
+      size_t& cur = g_smem_optin[std::make_pair((const void*)kernel, dev)];
+      if (smem > cur) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cur = smem;
+      }
+    }
   }
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
     per_sm = 0;

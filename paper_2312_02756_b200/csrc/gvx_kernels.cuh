@@ -360,7 +360,10 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(con
       int it = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int s = it % CFG::STAGES, k = it / CFG::STAGES;
-        if (k > 0) tma::mbar_wait(&empty[s], (k - 1) & 1);
+        if (k > 0) {
+          tma::mbar_wait(&empty[s], (k - 1) & 1);
+          tma::fence_proxy_async_smem();  // consumers' reads before the async-proxy refill
+        }
         tma::mbar_arrive_expect_tx(&full[s], CFG::STAGE_BYTES);
         T* dst = ring + (size_t)s * 2 * TV;
         tma::bulk_g2s(dst, v1 + t * TV, CFG::HALF, &full[s], pol);
@@ -380,6 +383,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(con
         lds_vec(src, u * CFG::NCT + ctid, lane, a[u]);
         lds_vec(src + TV, u * CFG::NCT + ctid, lane, b[u]);
       }
+      tma::fence_proxy_async_smem();  // this stage's LDS are performed before its release
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
 #pragma unroll

@@ -380,7 +380,7 @@ def test_tma_ring_kernels_all_modes():
     env = dict(os.environ, GVX_FORCE_TMA="1")
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", os.path.join(here, "test_gpu_parity.py"),
-                        "-k", "cfg1 or layouts or small_and_empty or histogram_parity or single_bin or nbins"],
+                        "-k", "cfg1 or layouts or small_and_empty or histogram_parity or single_bin or nbins or deterministic"],
                        env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
@@ -423,3 +423,20 @@ def test_boosted_output_f32(gvx, O):
     ok = np.isfinite(bref).all(1) & (np.abs(mlab) >= 1e-2 * e)
     S = (e[ok].astype(np.float64) ** 2) / np.abs(mlab[ok].astype(np.float64))
     assert (np.abs(bg[ok] - bref[ok]).max(1) / S).max() <= 1e-4
+
+
+@pytest.mark.parametrize("dt", [torch.float64, torch.float32])
+def test_repeat_runs_bitwise_deterministic(gvx, dt):
+    """Same inputs, same bits, run after run — on L2-resident inputs (1M pairs), where a
+    premature reuse of a TMA ring stage would show up (regression test for the missing
+    generic->async proxy fence found in round 1)."""
+    import synth.device as sd
+    n = (1 << 20) + 12345
+    v1, v2 = sd.muon_pairs(n, dtype=dt)
+    m0 = gvx.invariant_mass(v1, v2)
+    h0 = gvx.mass_histogram(v1, v2)
+    c0 = gvx.mass_histogram(v1, v2, cm=True)
+    for _ in range(12):
+        assert torch.equal(gvx.invariant_mass(v1, v2), m0)
+        assert torch.equal(gvx.mass_histogram(v1, v2), h0)
+        assert torch.equal(gvx.mass_histogram(v1, v2, cm=True), c0)

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1)) ring(const char* __restrict__ 
       tma::mbar_wait(&full[s], k & 1);
       const int4* p = reinterpret_cast<const int4*>(smem + s * STAGE);
       for (int i = ct; i < STAGE / 16; i += NCW * 32) { int4 v = p[i]; acc ^= v.x ^ v.y ^ v.z ^ v.w; }
+      tma::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
     }
