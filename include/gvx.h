@@ -33,8 +33,9 @@
  *     AoS [N][4]:        c[k] = base + k,     stride = 4
  *     SoA 4 x [N]:       c[k] = array_k,      stride = 1
  *     pairs [N][2][4]:   v1.c[k] = base + k, v2.c[k] = base + 4 + k, stride = 8
- *   Component order is (pt, eta, phi, m) for GVX_PTETAPHIM and (px, py, pz, E)
- *   for GVX_PXPYPZE (E last). Any view is accepted; AoS with
+ *   Component order is (pt, eta, phi, m) for GVX_PTETAPHIM, (px, py, pz, E) for
+ *   GVX_PXPYPZE (E last), (px, py, pz, m) for GVX_PXPYPZM and
+ *   (pt, eta, phi, E) for GVX_PTETAPHIE. Any view is accepted; AoS with
  *   4*sizeof(T) alignment and SoA with 16-byte-aligned arrays take the
  *   vectorised fast paths. Results are bitwise identical across layouts.
  */
@@ -62,8 +63,10 @@ typedef enum {
 typedef enum { GVX_F32 = 0, GVX_F64 = 1 } gvx_dtype;
 
 /* 4D coordinate systems ("any 4-dimensional
- * coordinate system"). Mass and histogram accept both; boost takes PXPYPZE. */
-typedef enum { GVX_PTETAPHIM = 0, GVX_PXPYPZE = 1 } gvx_coords;
+ * coordinate system"). Mass and histogram accept all four (conversions to
+ * PxPyPzE: SPEC.md:81 for pt/eta/phi, E = sqrt(|p|^2 + m|m|) clamped at 0 for
+ * a mass coordinate, R2); boost takes PXPYPZE. */
+typedef enum { GVX_PTETAPHIM = 0, GVX_PXPYPZE = 1, GVX_PXPYPZM = 2, GVX_PTETAPHIE = 3 } gvx_coords;
 
 typedef struct { const void *c[4]; int64_t stride; } gvx_vec4_cview;
 typedef struct { void *c[4]; int64_t stride; } gvx_vec4_view;

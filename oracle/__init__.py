@@ -23,7 +23,9 @@ _SOURCES = ["gvx_oracle.c", "gvx_oracle_body.inc", "gvx_oracle.h"]
 
 PTETAPHIM = 0
 PXPYPZE = 1
-_COORDS = {"ptetaphim": PTETAPHIM, "pxpypze": PXPYPZE}
+PXPYPZM = 2
+PTETAPHIE = 3
+_COORDS = {"ptetaphim": PTETAPHIM, "pxpypze": PXPYPZE, "pxpypzm": PXPYPZM, "ptetaphie": PTETAPHIE}
 
 
 def build(force: bool = False) -> str:

@@ -19,7 +19,8 @@
 extern "C" {
 #endif
 
-enum { GVX_REF_PTETAPHIM = 0, GVX_REF_PXPYPZE = 1 };
+/* 4D coordinate systems: component order of a vector. */
+enum { GVX_REF_PTETAPHIM = 0, GVX_REF_PXPYPZE = 1, GVX_REF_PXPYPZM = 2, GVX_REF_PTETAPHIE = 3 };
 enum { GVX_REF_DOMAIN = 2 };
 
 /* ROOT TH1 FindBin on a uniform axis (reading R12): 0 = underflow,

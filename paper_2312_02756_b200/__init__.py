@@ -16,7 +16,8 @@ Names follow the paper ("InvariantMasses", "ApplyBoost"):
 Vector arguments are CUDA tensors ``[N, 4]`` (AoS, any row stride — e.g. the
 ``[:, 0, :]`` view of interleaved ``[N, 2, 4]`` pairs) or a 4-sequence of
 ``[N]`` tensors sharing one stride (SoA). Components are (pt, eta, phi, m)
-for ``coords="ptetaphim"`` and (px, py, pz, E) for ``coords="pxpypze"``.
+for ``coords="ptetaphim"``, (px, py, pz, E) for ``"pxpypze"``, (px, py, pz, m)
+for ``"pxpypzm"`` and (pt, eta, phi, E) for ``"ptetaphie"``.
 """
 from __future__ import annotations
 
@@ -39,6 +40,8 @@ GVX_F32 = 0
 GVX_F64 = 1
 GVX_PTETAPHIM = 0
 GVX_PXPYPZE = 1
+GVX_PXPYPZM = 2
+GVX_PTETAPHIE = 3
 GVX_HIST_BOOST_TO_CM = 0x1
 ABI_VERSION = 1
 
@@ -128,9 +131,10 @@ def _dtype_code(dt: torch.dtype) -> int:
 
 def _coords_code(coords: str) -> int:
     try:
-        return {"ptetaphim": GVX_PTETAPHIM, "pxpypze": GVX_PXPYPZE}[coords]
+        return {"ptetaphim": GVX_PTETAPHIM, "pxpypze": GVX_PXPYPZE, "pxpypzm": GVX_PXPYPZM,
+                "ptetaphie": GVX_PTETAPHIE}[coords]
     except KeyError:
-        raise ValueError(f"coords must be 'ptetaphim' or 'pxpypze', got {coords!r}") from None
+        raise ValueError(f"coords must be one of ptetaphim, pxpypze, pxpypzm, ptetaphie; got {coords!r}") from None
 
 
 def _require_cuda(t: torch.Tensor, name: str) -> None:

@@ -93,7 +93,9 @@ inline bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 size_t dsize(gvx_dtype d) { return d == GVX_F64 ? 8 : 4; }
 
 bool valid_dtype(gvx_dtype d) { return d == GVX_F32 || d == GVX_F64; }
-bool valid_coords(gvx_coords c) { return c == GVX_PTETAPHIM || c == GVX_PXPYPZE; }
+bool valid_coords(gvx_coords c) {
+  return c == GVX_PTETAPHIM || c == GVX_PXPYPZE || c == GVX_PXPYPZM || c == GVX_PTETAPHIE;
+}
 
 template <int NC, typename V>
 bool view_ok(const V* v, size_t es) {
@@ -278,10 +280,12 @@ gvx_status dispatch_mass(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, voi
   int L = (l1 == l2) ? l1 : L_GEN;
   if (L == L_AOS && !aligned(m, Group<T, L_AOS>::G * sizeof(T))) L = L_GEN;  // vector stores
   if (L == L_SOA && !aligned(m, Group<T, L_SOA>::G * sizeof(T))) L = L_GEN;
-  if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, PM_MASS>()) {
-    HistParams hp{};
-    gvx_status st = launch_pair_tma<T, C, PM_MASS>(v1, v2, n, m, hp, nullptr, nullptr, s);
-    if (st != GVX_ERR_UNSUPPORTED) return st;
+  if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
+    if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, PM_MASS>()) {
+      HistParams hp{};
+      gvx_status st = launch_pair_tma<T, C, PM_MASS>(v1, v2, n, m, hp, nullptr, nullptr, s);
+      if (st != GVX_ERR_UNSUPPORTED) return st;
+    }
   }
   if (L == L_AOS) return launch_mass<T, C, L_AOS>(v1, v2, m, n, s);
   if (L == L_SOA) return launch_mass<T, C, L_SOA>(v1, v2, m, n, s);
@@ -377,9 +381,11 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
       return launch_hist<T, C, L_GEN, CM, true>(v1, v2, n, hp, bins, m_out, bo, s);
     }
   }
-  if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, CM ? PM_HIST_CM : PM_HIST>()) {
-    gvx_status st = launch_pair_tma<T, C, CM ? PM_HIST_CM : PM_HIST>(v1, v2, n, m_out, hp, bins, nullptr, s);
-    if (st != GVX_ERR_UNSUPPORTED) return st;
+  if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
+    if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, CM ? PM_HIST_CM : PM_HIST>()) {
+      gvx_status st = launch_pair_tma<T, C, CM ? PM_HIST_CM : PM_HIST>(v1, v2, n, m_out, hp, bins, nullptr, s);
+      if (st != GVX_ERR_UNSUPPORTED) return st;
+    }
   }
   if (L == L_AOS) return launch_hist<T, C, L_AOS, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
   if (L == L_SOA) return launch_hist<T, C, L_SOA, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
@@ -412,11 +418,18 @@ gvx_status gvx_invariant_mass(gvx_dtype dtype, gvx_coords coords, const gvx_vec4
   size_t es = dsize(dtype);
   if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !m_out || !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == GVX_F64)
-    return coords == GVX_PTETAPHIM ? dispatch_mass<double, C_PTETAPHIM>(v1, v2, m_out, n, s)
-                                   : dispatch_mass<double, C_PXPYPZE>(v1, v2, m_out, n, s);
-  return coords == GVX_PTETAPHIM ? dispatch_mass<float, C_PTETAPHIM>(v1, v2, m_out, n, s)
-                                 : dispatch_mass<float, C_PXPYPZE>(v1, v2, m_out, n, s);
+#define GVX_MASS_DISPATCH(T)                                                     \
+  switch (coords) {                                                             \
+    case GVX_PTETAPHIM: return dispatch_mass<T, C_PTETAPHIM>(v1, v2, m_out, n, s); \
+    case GVX_PXPYPZE: return dispatch_mass<T, C_PXPYPZE>(v1, v2, m_out, n, s);     \
+    case GVX_PXPYPZM: return dispatch_mass<T, C_PXPYPZM>(v1, v2, m_out, n, s);     \
+    default: return dispatch_mass<T, C_PTETAPHIE>(v1, v2, m_out, n, s);          \
+  }
+  if (dtype == GVX_F64) {
+    GVX_MASS_DISPATCH(double)
+  }
+  GVX_MASS_DISPATCH(float)
+#undef GVX_MASS_DISPATCH
 }
 
 gvx_status gvx_boost(gvx_dtype dtype, const gvx_vec4_cview* v, const gvx_vec3_cview* beta, const gvx_vec4_view* out,
@@ -466,8 +479,18 @@ gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4
 #define GVX_HIST_DISPATCH(T, C)                                                                                  \
   (cm ? dispatch_hist<T, C, true>(v1, v2, n, hp, bins, m_out, boosted_out, s)                       \
       : dispatch_hist<T, C, false>(v1, v2, n, hp, bins, m_out, boosted_out, s))
-  if (dtype == GVX_F64) return coords == GVX_PTETAPHIM ? GVX_HIST_DISPATCH(double, C_PTETAPHIM) : GVX_HIST_DISPATCH(double, C_PXPYPZE);
-  return coords == GVX_PTETAPHIM ? GVX_HIST_DISPATCH(float, C_PTETAPHIM) : GVX_HIST_DISPATCH(float, C_PXPYPZE);
+#define GVX_HIST_COORDS(T)                                            \
+  switch (coords) {                                                  \
+    case GVX_PTETAPHIM: return GVX_HIST_DISPATCH(T, C_PTETAPHIM);    \
+    case GVX_PXPYPZE: return GVX_HIST_DISPATCH(T, C_PXPYPZE);        \
+    case GVX_PXPYPZM: return GVX_HIST_DISPATCH(T, C_PXPYPZM);        \
+    default: return GVX_HIST_DISPATCH(T, C_PTETAPHIE);               \
+  }
+  if (dtype == GVX_F64) {
+    GVX_HIST_COORDS(double)
+  }
+  GVX_HIST_COORDS(float)
+#undef GVX_HIST_COORDS
 #undef GVX_HIST_DISPATCH
 }
 

@@ -19,7 +19,7 @@
 namespace gvx {
 
 enum Layout { L_AOS = 0, L_SOA = 1, L_GEN = 2 };
-enum Coords { C_PTETAPHIM = 0, C_PXPYPZE = 1 };
+enum Coords { C_PTETAPHIM = 0, C_PXPYPZE = 1, C_PXPYPZM = 2, C_PTETAPHIE = 3 };
 
 template <typename T> struct View4 { const T* c[4]; int64_t s; };
 template <typename T> struct View4o { T* c[4]; int64_t s; };
@@ -94,19 +94,22 @@ __device__ __forceinline__ void store_group(T* __restrict__ out, int64_t g, cons
 }
 
 template <typename T, int COORDS>
-__device__ __forceinline__ T event_mass(const T (&a)[4], const T (&b)[4]) {
-  if constexpr (COORDS == C_PTETAPHIM) {
-    return pair_mass_ptetaphim(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3]);
-  } else {
-    V4<T> x{a[0], a[1], a[2], a[3]}, y{b[0], b[1], b[2], b[3]};
-    return mass_of_sum(x, y);
-  }
+__device__ __forceinline__ V4<T> to_cartesian(const T (&a)[4]) {
+  if constexpr (COORDS == C_PTETAPHIM) return ptetaphim_to_cartesian(a[0], a[1], a[2], a[3]);
+  else if constexpr (COORDS == C_PXPYPZM) return pxpypzm_to_cartesian(a[0], a[1], a[2], a[3]);
+  else if constexpr (COORDS == C_PTETAPHIE) return ptetaphie_to_cartesian(a[0], a[1], a[2], a[3]);
+  else return V4<T>{a[0], a[1], a[2], a[3]};
 }
 
 template <typename T, int COORDS>
-__device__ __forceinline__ V4<T> to_cartesian(const T (&a)[4]) {
-  if constexpr (COORDS == C_PTETAPHIM) return ptetaphim_to_cartesian(a[0], a[1], a[2], a[3]);
-  else return V4<T>{a[0], a[1], a[2], a[3]};
+__device__ __forceinline__ T event_mass(const T (&a)[4], const T (&b)[4]) {
+  if constexpr (COORDS == C_PTETAPHIM) {
+    return pair_mass_ptetaphim(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3]);
+  } else if constexpr (COORDS == C_PTETAPHIE) {
+    return pair_mass_ptetaphie(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3]);
+  } else {
+    return mass_of_sum(to_cartesian<T, COORDS>(a), to_cartesian<T, COORDS>(b));
+  }
 }
 
 // ============================================================================
@@ -209,7 +212,7 @@ __device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], i
       M = cm_pair_mass(ptetaphim_exact(a[0], a[1], a[2], a[3]), ptetaphim_exact(b[0], b[1], b[2], b[3]),
                        WANT_BO ? &xa : nullptr, &yb);
     } else {
-      M = cm_pair_mass(V4<T>{a[0], a[1], a[2], a[3]}, V4<T>{b[0], b[1], b[2], b[3]}, WANT_BO ? &xa : nullptr, &yb);
+      M = cm_pair_mass(to_cartesian<T, COORDS>(a), to_cartesian<T, COORDS>(b), WANT_BO ? &xa : nullptr, &yb);
     }
     if constexpr (WANT_BO) {
       int64_t j0 = (2 * i) * bo.s, j1 = (2 * i + 1) * bo.s;

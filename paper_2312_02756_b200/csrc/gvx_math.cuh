@@ -499,6 +499,58 @@ __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1,
 }
 
 // ---------------------------------------------------------------------------
+// PxPyPzM and PtEtaPhiE.
+// ---------------------------------------------------------------------------
+// PxPyPzM -> PxPyPzE: E = sqrt(max(0, |p|^2 + m|m|)) (R2 clamp).
+template <typename T>
+__device__ __forceinline__ V4<T> pxpypzm_to_cartesian(T px, T py, T pz, T m) {
+  T e2 = px * px + py * py + pz * pz + m * (m < T(0) ? -m : m);
+  return V4<T>{px, py, pz, ieee_sqrt(e2 > T(0) ? e2 : T(0))};
+}
+
+// PtEtaPhiE -> PxPyPzE with accurate libm (cold path).
+__device__ __noinline__ V4<double> ptetaphie_exact(double pt, double eta, double phi, double E) {
+  double s, c;
+  sincos(phi, &s, &c);
+  return V4<double>{pt * c, pt * s, pt * sinh(eta), E};
+}
+__device__ __noinline__ V4<float> ptetaphie_exact(float pt, float eta, float phi, float E) {
+  float s, c;
+  sincosf(phi, &s, &c);
+  return V4<float>{pt * c, pt * s, pt * sinhf(eta), E};
+}
+// Fast domain for PtEtaPhiE: the angle/rapidity limits of PtEtaPhiM and a finite E.
+template <typename T>
+__device__ __forceinline__ bool fast_domain_e(T pt, T eta, T phi, T E) {
+  return fast_domain(pt, eta, phi, T(0)) && fabs(E) < T(1e30);
+}
+template <typename T>
+__device__ __forceinline__ V4<T> ptetaphie_to_cartesian(T pt, T eta, T phi, T E) {
+  if (fast_domain_e(pt, eta, phi, E)) {
+    T s, c, sh, ch;
+    fast_sincos(phi, s, c);
+    sinh_cosh(eta, sh, ch);
+    return V4<T>{pt * c, pt * s, pt * sh, E};
+  }
+  return ptetaphie_exact(pt, eta, phi, E);
+}
+// Pair mass of PtEtaPhiE vectors without forming Cartesian vectors:
+//   M^2 = (E1 + E2)^2 - (pt1 ch1)^2 - (pt2 ch2)^2 - 2 pt1 pt2 (cos(phi1 - phi2) + sh1 sh2)
+template <typename T>
+__device__ __forceinline__ T pair_mass_ptetaphie(T pt1, T eta1, T phi1, T E1, T pt2, T eta2, T phi2, T E2) {
+  if (fast_domain_e(pt1, eta1, phi1, E1) && fast_domain_e(pt2, eta2, phi2, E2)) {
+    T sd, c, sh1, ch1, sh2, ch2;
+    fast_sincos(phi1 - phi2, sd, c);
+    sinh_cosh(eta1, sh1, ch1);
+    sinh_cosh(eta2, sh2, ch2);
+    T q1 = pt1 * ch1, q2 = pt2 * ch2, E = E1 + E2;
+    T m2 = E * E - q1 * q1 - q2 * q2 - T(2) * pt1 * pt2 * (c + sh1 * sh2);
+    return fast_signed_sqrt(m2);
+  }
+  return mass_of_sum(ptetaphie_exact(pt1, eta1, phi1, E1), ptetaphie_exact(pt2, eta2, phi2, E2));
+}
+
+// ---------------------------------------------------------------------------
 // ROOT FindFixBin in double, bit-identical to the oracle's
 //   1 + (int)((nbins * (x - lo)) / (hi - lo))
 // The quotient is first formed with a precomputed reciprocal (error a few

@@ -440,3 +440,51 @@ def test_repeat_runs_bitwise_deterministic(gvx, dt):
         assert torch.equal(gvx.invariant_mass(v1, v2), m0)
         assert torch.equal(gvx.mass_histogram(v1, v2), h0)
         assert torch.equal(gvx.mass_histogram(v1, v2, cm=True), c0)
+
+
+def other_coords_inputs(n, dt, coords, seed=31):
+    """Seeded pairs in PxPyPzM / PtEtaPhiE (built on the host from synth muons; both sides
+    receive the same rounded values)."""
+    v1, v2 = synth.muon_pairs(np.arange(n), seed=seed)
+    out = []
+    for v in (v1, v2):
+        pt, eta, phi, m = v.T
+        if coords == "pxpypzm":
+            w = np.stack([pt * np.cos(phi), pt * np.sin(phi), pt * np.sinh(eta), m], 1)
+        else:
+            w = np.stack([pt, eta, phi, np.sqrt(m * m + (pt * np.cosh(eta)) ** 2)], 1)
+        out.append(w.astype(dt))
+    # degenerate rows: spacelike / clamped masses, zero vectors, out-of-fast-domain eta
+    extra = np.array([[3, 4, 12, -5], [3, 4, 12, -20], [0, 0, 0, 0], [1, 25.0, 0.3, 5e10]], np.float64).astype(dt)
+    return np.concatenate([extra, out[0]]), np.concatenate([extra[::-1], out[1]])
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("coords", ["pxpypzm", "ptetaphie"])
+def test_other_coordinate_systems(gvx, O, dt, coords):
+    v1, v2 = other_coords_inputs(150_001, dt, coords)
+    mo, _ = O.invariant_mass(v1, v2, coords=coords)
+    # tolerance scale: sum of max(E_i, |p_i|) from the oracle's own E and |p| (R5)
+    z = np.zeros_like(v1)
+    _, e1 = O.invariant_mass(v1, z, coords=coords)
+    _, e2 = O.invariant_mass(v2, z, coords=coords)
+    a, b = v1.astype(np.float64), v2.astype(np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        p1 = np.sqrt((a[:, :3] ** 2).sum(1)) if coords == "pxpypzm" else np.abs(a[:, 0]) * np.cosh(a[:, 1])
+        p2 = np.sqrt((b[:, :3] ** 2).sum(1)) if coords == "pxpypzm" else np.abs(b[:, 0]) * np.cosh(b[:, 1])
+    e = np.fmax(e1.astype(np.float64), p1) + np.fmax(e2.astype(np.float64), p2)
+    tau = tau_of(dt)
+    t1, t2 = dev(v1), dev(v2)
+    m = host(gvx.invariant_mass(t1, t2, coords=coords))
+    bad = mass_violations(m, mo, e, tau)
+    assert bad.size == 0, (bad[:5], m[bad[:5]], mo[bad[:5]])
+    m_soa = host(gvx.invariant_mass([t1[:, k].contiguous() for k in range(4)],
+                                    [t2[:, k].contiguous() for k in range(4)], coords=coords))
+    assert np.array_equal(m_soa, m, equal_nan=True)
+    for cm in (False, True):
+        h = host(gvx.mass_histogram(t1, t2, coords=coords, cm=cm))
+        ho, mho = O.mass_histogram(v1, v2, LO, HI, NB, cm=cm, coords=coords)
+        mlab = mo
+        nanp = (np.isnan(mho) | (np.abs(mlab.astype(np.float64)) < (1e-2 if dt == np.float32 else 1e-6) * e)) if cm else None
+        fails, _ = hist_check(h, mho, e, tau, LO, HI, NB, nan_possible=nanp, m_window_center=mlab if cm else None)
+        assert not fails, (cm, fails)

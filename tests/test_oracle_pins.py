@@ -416,3 +416,59 @@ def test_histogram_single_bin_stress(O):
     bins, _ = O.mass_histogram(v, v, 0.25, 300.0, 1000, coords="pxpypze")
     b = brute_bin(91.0, 0.25, 300.0, 1000)
     assert bins[b] == 1000 and bins.sum() == 1000
+
+
+# --------------------------------------------------------------------------
+# Other 4D coordinate systems
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_pxpypzm_closed_forms(O, dt):
+    z = np.zeros((1, 4), dt)
+    # |p| = 13 (3-4-12): m = 0 -> lightlike; m = 5 -> E = sqrt(194), mass 5
+    m, e = O.invariant_mass(np.array([[3, 4, 12, 0]], dt), z, coords="pxpypzm")
+    assert m[0] == 0 and e[0] == 13
+    m, e = O.invariant_mass(np.array([[3, 4, 12, 5]], dt), z, coords="pxpypzm")
+    assert m[0] == pytest.approx(5, rel=8 * np.finfo(dt).eps) and e[0] == dt(np.sqrt(194.0))
+    # spacelike m = -5: E^2 = 169 - 25 = 144 -> M = -5 (R3/R4)
+    m, e = O.invariant_mass(np.array([[3, 4, 12, -5]], dt), z, coords="pxpypzm")
+    assert e[0] == 12 and m[0] == pytest.approx(-5, rel=8 * np.finfo(dt).eps)
+    # clamp (R2): m = -20 -> E = 0, M = -|p| = -13
+    m, e = O.invariant_mass(np.array([[3, 4, 12, -20]], dt), z, coords="pxpypzm")
+    assert e[0] == 0 and m[0] == -13
+
+
+def test_coordinate_systems_agree(O):
+    """The same physical pairs written in all four systems give the same mass (mpmath
+    conversions at 40 digits, independent of the oracle's own conversion code)."""
+    v1, v2 = synth.muon_pairs(np.arange(300), seed=13)
+    def forms(v):
+        out = {k: [] for k in ("ptetaphim", "pxpypze", "pxpypzm", "ptetaphie")}
+        for pt, eta, phi, m in v:
+            pt, eta, phi, m = (mp.mpf(float(x)) for x in (pt, eta, phi, m))
+            px, py, pz = pt * mp.cos(phi), pt * mp.sin(phi), pt * mp.sinh(eta)
+            E = mp.sqrt(m * m + px * px + py * py + pz * pz)
+            out["ptetaphim"].append([float(pt), float(eta), float(phi), float(m)])
+            out["pxpypze"].append([float(px), float(py), float(pz), float(E)])
+            out["pxpypzm"].append([float(px), float(py), float(pz), float(m)])
+            out["ptetaphie"].append([float(pt), float(eta), float(phi), float(E)])
+        return {k: np.array(x) for k, x in out.items()}
+    f1, f2 = forms(v1), forms(v2)
+    ref, e = O.invariant_mass(f1["ptetaphim"], f2["ptetaphim"])
+    for c in ("pxpypze", "pxpypzm", "ptetaphie"):
+        m, _ = O.invariant_mass(f1[c], f2[c], coords=c)
+        assert np.max(np.abs(m * np.abs(m) - ref * np.abs(ref)) / e ** 2) <= 1e-14, c
+        mc, _ = O.cm_mass(f1[c], f2[c], coords=c)
+        assert np.max(np.abs(mc * np.abs(mc) - ref * np.abs(ref)) / e ** 2) <= 1e-13, c
+
+
+def test_ptetaphie_single_vector_mpmath(O):
+    rng = np.random.default_rng(17)
+    v = np.stack([rng.uniform(1, 100, 100), rng.uniform(-3, 3, 100), rng.uniform(-np.pi, np.pi, 100),
+                  np.zeros(100)], 1)
+    v[:, 3] = v[:, 0] * np.cosh(v[:, 1]) * rng.uniform(1.0, 1.5, 100)  # timelike E
+    m, e = O.invariant_mass(v, np.zeros_like(v), coords="ptetaphie")
+    for i in range(100):
+        pt, eta, E = (mp.mpf(float(x)) for x in (v[i, 0], v[i, 1], v[i, 3]))
+        M2 = E * E - (pt * mp.cosh(eta)) ** 2
+        assert abs(mp.mpf(float(m[i])) ** 2 - M2) <= 1e-14 * E * E
