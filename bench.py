@@ -316,6 +316,8 @@ def run_ours(args):
         kernels[k] = {"ms": avg, "events_per_s": n / (avg * 1e-3), "bytes_per_event": bpe,
                       "achieved_GBs": gbs, "frac_of_peak": gbs / peak}
     dom = max(KERNEL_ORDER, key=lambda k: kernels[k]["ms"])
+    step_bytes = n * sum(BYTES[k](es) for k in KERNEL_ORDER)
+    step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9  # per GPU: each rank moves step_bytes
     roofline = {"bound": "hbm", "kernel": f"gvx_{dom}", "achieved": kernels[dom]["achieved_GBs"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dom]["frac_of_peak"], "traffic": ncu_traffic(dom, args.dtype, n),
                 "peak_source": peak_kind,
@@ -339,6 +341,8 @@ def run_ours(args):
             "config": config_obj(args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk.summary(), "kernels": kernels,
+            "step_hbm": {"algorithmic_bytes_per_gpu": step_bytes, "achieved_GBs_per_gpu": step_gbs,
+                         "frac_of_peak": step_gbs / peak, "peak": peak},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

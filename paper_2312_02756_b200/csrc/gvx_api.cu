@@ -238,6 +238,8 @@ gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, i
       case 9: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 992, 3, 31, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
       case 10: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 448, 3, 14, 2>>(v1, v2, n, m_out, hp, bins, bo, s);
       case 11: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 896, 2, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 12: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1024, 3, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 13: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1280, 2, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
       default: break;
     }
   }
