@@ -52,6 +52,11 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=1 << 22, help="events in the oracle's bounded sample")
     p.add_argument("--dist-backend", default="nccl", help="process-group backend for N>1 (nccl on B200s)")
+    p.add_argument("--sweep", action="store_true", help="N sweep (CFG2 shape) instead of the step benchmark")
+    p.add_argument("--extended", action="store_true",
+                   help="also time the widened rows (other coordinate systems, SoA, uniform boost) at N")
+    p.add_argument("--sweep-out", default=os.path.join(ROOT, "gpurun_out", "nsweep.jsonl"))
+    p.add_argument("--sweep-reps", type=int, default=10)
     return p.parse_args()
 
 
@@ -323,6 +328,8 @@ def run_ours(args):
                 "peak_source": peak_kind,
                 "bytes_per_launch": n * BYTES[dom](es)}
 
+    extended = run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak) if args.extended else None
+
     # e2e: the same step from pinned HOST buffers through the public API, copies timed
     e2e = None
     if not args.no_e2e:
@@ -343,10 +350,49 @@ def run_ours(args):
             "gpu_launches": 4 * args.steps, "clocks": clk.summary(), "kernels": kernels,
             "step_hbm": {"algorithmic_bytes_per_gpu": step_bytes, "achieved_GBs_per_gpu": step_gbs,
                          "frac_of_peak": step_gbs / peak, "peak": peak},
+            **({"extended": extended} if extended else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
+    """Widened rows on the same N: the mass in the other coordinate systems
+    (the PtEtaPhiM vectors reinterpreted — same bytes, same branch-free fast domain), SoA
+    views, and the paper's single-matrix ApplyBoost. CUDA events, mean of --steps launches."""
+    import torch
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / args.steps
+
+    s1 = [v1[:, k].contiguous() for k in range(4)]
+    s2 = [v2[:, k].contiguous() for k in range(4)]
+    cases = {
+        "mass_pxpypze": (lambda: gvx.invariant_mass(v1, v2, out=m, coords="pxpypze"), 9 * es),
+        "mass_pxpypzm": (lambda: gvx.invariant_mass(v1, v2, out=m, coords="pxpypzm"), 9 * es),
+        "mass_ptetaphie": (lambda: gvx.invariant_mass(v1, v2, out=m, coords="ptetaphie"), 9 * es),
+        "mass_soa": (lambda: gvx.invariant_mass(s1, s2, out=m), 9 * es),
+        "hist_soa": (lambda: gvx.mass_histogram(s1, s2), 8 * es),
+        "boost_uniform": (lambda: gvx.boost_uniform(bv, (0.3, -0.4, 0.5), out=bout), 8 * es),
+    }
+    out = {}
+    for k, (fn, bpe) in cases.items():
+        ms = timed(fn)
+        gbs = n * bpe / (ms * 1e-3) / 1e9
+        out[k] = {"ms": ms, "events_per_s": n / (ms * 1e-3), "bytes_per_event": bpe, "achieved_GBs": gbs,
+                  "frac_of_peak": gbs / peak}
+    del s1, s2
+    return out
 
 
 def ncu_traffic(kernel: str, dtype: str, n: int):
@@ -401,8 +447,108 @@ def run_e2e(args, gvx, v1, v2, bv, bb, dev, stream, world):
             "steps": steps, "path": "pinned host -> chunked H2D/compute/D2H over 2 streams (hostpipe)"}
 
 
+
+# ----------------------------------------------------------------------------
+# --sweep: CFG2 and the paper's own experiment shape: mass
+# (AoS, SoA) and boost over N = 1e4..1e8, f64 and f32, L2 flushed between
+# repetitions, with the paper's metric — speedup over the single-threaded CPU
+# run — against the oracle on this host (measured to N = 1e6, extrapolated
+# linearly above and marked so). One JSON line per point.
+# ----------------------------------------------------------------------------
+SWEEP_NS = [10_000, 30_000, 100_000, 300_000, 1_000_000, 3_000_000, 10_000_000, 30_000_000, 100_000_000]
+
+
+def gpu_time(fn, reps, flush):
+    import statistics
+
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    fn()
+    torch.cuda.synchronize()
+    for a, b in ev:
+        flush.fill_(1)  # 512 MB write: evicts the 126 MB L2
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    ts = [a.elapsed_time(b) for a, b in ev]
+    return min(ts), statistics.median(ts)
+
+
+def cpu_time(fn, reps=3):
+    import time
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        best = min(best, time.perf_counter() - t0)
+    return best * 1e3
+
+
+def run_sweep(args):
+    """`--sweep`: CFG2 / the paper's experiment shape (speedup over one CPU thread vs N)."""
+    import numpy as np
+    import torch
+
+    import oracle  # the CPU baseline of each sweep point (cpu_baseline leg)
+    import paper_2312_02756_b200 as gvx
+    import synth
+    import synth.device as sd
+    out_path = args.sweep_out
+    reps = args.sweep_reps
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    cpu_ms_per_event = {}
+    with open(out_path, "w") as f:
+        for dtn, tdt, npdt, es in (("f64", torch.float64, np.float64, 8), ("f32", torch.float32, np.float32, 4)):
+            # oracle 1-thread cost per event (mass and boost), from N = 1e6 (paper's baseline)
+            idx = np.arange(1_000_000)
+            h1, h2 = synth.muon_pairs(idx, dtype=npdt)
+            hv, hb = synth.boost_inputs(idx, dtype=npdt)
+            cpu_ms_per_event[dtn] = {"mass": cpu_time(lambda: oracle.invariant_mass(h1, h2)) / 1e6,
+                                     "boost": cpu_time(lambda: oracle.boost(hv, hb)) / 1e6}
+            for n in SWEEP_NS:
+                v1, v2 = sd.muon_pairs(n, dtype=tdt)
+                bv, bb = sd.boost_inputs(n, dtype=tdt)
+                m = torch.empty(n, dtype=tdt, device="cuda")
+                out = torch.empty((n, 4), dtype=tdt, device="cuda")
+                s1 = [v1[:, k].contiguous() for k in range(4)]
+                s2 = [v2[:, k].contiguous() for k in range(4)]
+                cases = [
+                    ("mass", "AoS", lambda: gvx.invariant_mass(v1, v2, out=m), 9 * es),
+                    ("mass", "SoA", lambda: gvx.invariant_mass(s1, s2, out=m), 9 * es),
+                    ("boost", "AoS", lambda: gvx.boost(bv, bb, out=out), 11 * es),
+                ]
+                for what, layout, fn, bpe in cases:
+                    best, med = gpu_time(fn, reps, flush)
+                    if n <= 1_000_000:
+                        ii = np.arange(n)
+                        if what == "mass":
+                            a, b = synth.muon_pairs(ii, dtype=npdt)
+                            cpu = cpu_time(lambda: oracle.invariant_mass(a, b))
+                        else:
+                            a, b = synth.boost_inputs(ii, dtype=npdt)
+                            cpu = cpu_time(lambda: oracle.boost(a, b))
+                        cpu_kind = "measured"
+                    else:
+                        cpu = cpu_ms_per_event[dtn][what] * n
+                        cpu_kind = "extrapolated from N=1e6"
+                    rec = {"op": what, "dtype": dtn, "layout": layout, "n": n, "gpu_ms_best": best,
+                           "gpu_ms_median": med, "events_per_s": n / (best * 1e-3),
+                           "GBs": n * bpe / (best * 1e-3) / 1e9, "cpu_1thread_ms": cpu, "cpu_kind": cpu_kind,
+                           "speedup_vs_1thread": cpu / best, "l2": "flushed (512 MB write) before each rep"}
+                    f.write(json.dumps(rec) + "\n")
+                    f.flush()
+                    print(json.dumps(rec))
+                del v1, v2, bv, bb, m, out, s1, s2
+                torch.cuda.empty_cache()
+
+
+
 def main():
     args = parse()
+    if args.sweep:
+        run_sweep(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:
