@@ -196,10 +196,13 @@ template <typename T, int C, int MODE, typename CFG>
 gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, void* m_out,
                                const HistParams& hp, unsigned long long* bins, const gvx_vec4_view* bo,
                                cudaStream_t s) {
+  // AoS (paper layout) or SoA with 16-byte aligned component arrays; else not handled here.
+  const bool soa = classify(v1, sizeof(T)) == L_SOA && classify(v2, sizeof(T)) == L_SOA;
+  if (!soa && !(classify(v1, sizeof(T)) == L_AOS && classify(v2, sizeof(T)) == L_AOS)) return GVX_ERR_UNSUPPORTED;
   const int nbs = MODE == PM_MASS ? 0 : hp.nbins + 2;
   const size_t sm = CFG::smem_bytes(nbs);
   if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
-  auto k = k_pair_tma<T, C, MODE, CFG>;
+  auto k = soa ? k_pair_tma<T, C, MODE, CFG, false, true> : k_pair_tma<T, C, MODE, CFG, false, false>;
   const int block = 32 * (CFG::NCW + 1);
   int per_sm = blocks_per_sm(k, block, sm);
   if (per_sm < 1) return GVX_ERR_UNSUPPORTED;
@@ -214,8 +217,12 @@ gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v
     View4o<T> bo2 = bov;
     if (bo)
       for (int c = 0; c < 4; ++c) bo2.c[c] += 2 * off * bo2.s;
-    k<<<grid, block, sm, s>>>((const T*)v1->c[0] + 4 * off, (const T*)v2->c[0] + 4 * off, cn,
-                              m_out ? (T*)m_out + off : nullptr, hp, bins, bo2);
+    View4<T> a = mk4<T>(v1), b = mk4<T>(v2);
+    for (int c = 0; c < 4; ++c) {
+      a.c[c] += off * a.s;
+      b.c[c] += off * b.s;
+    }
+    k<<<grid, block, sm, s>>>(a, b, cn, m_out ? (T*)m_out + off : nullptr, hp, bins, bo2);
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GVX_OK : cuda_fail(e);
@@ -384,7 +391,8 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
     }
   }
   if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
-    if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, CM ? PM_HIST_CM : PM_HIST>()) {
+    if (((l1 == L_AOS && l2 == L_AOS) || (l1 == L_SOA && l2 == L_SOA)) && tma_enabled() &&
+        tma_preferred<T, CM ? PM_HIST_CM : PM_HIST>()) {
       gvx_status st = launch_pair_tma<T, C, CM ? PM_HIST_CM : PM_HIST>(v1, v2, n, m_out, hp, bins, nullptr, s);
       if (st != GVX_ERR_UNSUPPORTED) return st;
     }

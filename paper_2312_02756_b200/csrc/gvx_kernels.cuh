@@ -331,8 +331,11 @@ __device__ __forceinline__ void pair_consume(const T (&a)[4], const T (&b)[4], i
   }
 }
 
-template <typename T, int COORDS, int MODE, typename CFG, bool WANT_BO = false>
-__global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(const T* __restrict__ v1, const T* __restrict__ v2,
+// SOA = false: each stage holds the v1 and v2 AoS tiles (2 bulk copies);
+// SOA = true: the 8 component tiles of v1 and v2 (8 bulk copies), read back
+// lane-contiguously (LDS.64 / LDS.32, no bank conflicts).
+template <typename T, int COORDS, int MODE, typename CFG, bool WANT_BO = false, bool SOA = false>
+__global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(View4<T> v1, View4<T> v2,
                                                                  int64_t n, T* __restrict__ m_out, HistParams hp,
                                                                  unsigned long long* __restrict__ bins, View4o<T> bo) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -369,8 +372,16 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(con
         }
         tma::mbar_arrive_expect_tx(&full[s], CFG::STAGE_BYTES);
         T* dst = ring + (size_t)s * 2 * TV;
-        tma::bulk_g2s(dst, v1 + t * TV, CFG::HALF, &full[s], pol);
-        tma::bulk_g2s(dst + TV, v2 + t * TV, CFG::HALF, &full[s], pol);
+        if constexpr (SOA) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            tma::bulk_g2s(dst + c * CFG::TILE, v1.c[c] + t * CFG::TILE, CFG::HALF / 4, &full[s], pol);
+            tma::bulk_g2s(dst + TV + c * CFG::TILE, v2.c[c] + t * CFG::TILE, CFG::HALF / 4, &full[s], pol);
+          }
+        } else {
+          tma::bulk_g2s(dst, v1.c[0] + t * TV, CFG::HALF, &full[s], pol);
+          tma::bulk_g2s(dst + TV, v2.c[0] + t * TV, CFG::HALF, &full[s], pol);
+        }
       }
     }
   } else {  // consumers
@@ -383,8 +394,17 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(con
       T a[CFG::EPT][4], b[CFG::EPT][4];
 #pragma unroll
       for (int u = 0; u < CFG::EPT; ++u) {
-        lds_vec(src, u * CFG::NCT + ctid, lane, a[u]);
-        lds_vec(src + TV, u * CFG::NCT + ctid, lane, b[u]);
+        const int e = u * CFG::NCT + ctid;
+        if constexpr (SOA) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            a[u][c] = src[c * CFG::TILE + e];
+            b[u][c] = src[TV + c * CFG::TILE + e];
+          }
+        } else {
+          lds_vec(src, e, lane, a[u]);
+          lds_vec(src + TV, e, lane, b[u]);
+        }
       }
       tma::fence_proxy_async_smem();  // this stage's LDS are performed before its release
       __syncwarp();
@@ -398,8 +418,13 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(con
     if (blockIdx.x == gridDim.x - 1) {
       for (int64_t i = ntiles * CFG::TILE + ctid; i < n; i += CFG::NCT) {
         T a[4], b[4];
+        if constexpr (SOA) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) { a[c] = v1[4 * i + c]; b[c] = v2[4 * i + c]; }
+          for (int c = 0; c < 4; ++c) { a[c] = v1.c[c][i]; b[c] = v2.c[c][i]; }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) { a[c] = v1.c[0][4 * i + c]; b[c] = v2.c[0][4 * i + c]; }
+        }
         pair_consume<T, COORDS, MODE, WANT_BO>(a, b, i, m_out, sh_hist, hp, bo);
       }
     }

@@ -246,6 +246,12 @@ def test_histogram_parity(gvx, O, dt, cm):
     assert not fails, fails
     # the GPU's own bins agree exactly with binning its masses
     assert np.array_equal(h, np.bincount(find_bin_np(mg, LO, HI, NB), minlength=NB + 2))
+    # SoA views (TMA component tiles) and a strided view give the same bins
+    hs = host(gvx.mass_histogram([t1[:, k].contiguous() for k in range(4)], [t2[:, k].contiguous() for k in range(4)],
+                                 LO, HI, NB, cm=cm))
+    pairs = torch.stack([t1, t2], dim=1).contiguous()
+    hp = host(gvx.mass_histogram(pairs[:, 0, :], pairs[:, 1, :], LO, HI, NB, cm=cm))
+    assert np.array_equal(hs, h) and np.array_equal(hp, h)
     print(f"hist dt={dt.__name__} cm={cm}: ambiguous events {namb}, exact bins "
           f"{int((h == bins_o).sum())}/{NB + 2}")
     if cm and dt == np.float64:
