@@ -385,13 +385,27 @@ def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
         "hist_soa": (lambda: gvx.mass_histogram(s1, s2), 8 * es),
         "boost_uniform": (lambda: gvx.boost_uniform(bv, (0.3, -0.4, 0.5), out=bout), 8 * es),
     }
+    # jagged events (f4): 1 event per pair slot of the batch, ~1.1 muons/event on average
+    import synth.device as sd
+    jmu, jq, joff = sd.jagged_events(0, n, dtype=v1.dtype, device=v1.device)
+    kk = joff[1:] - joff[:-1]
+    two = (kk == 2)
+    n_k2 = int(two.sum().item())
+    first = joff[:-1][two]
+    n_sel = int((jq[first] * jq[first + 1] < 0).sum().item())
+    del kk, two, first
+    cases["dimuon_jagged"] = (lambda: gvx.dimuon_histogram(jmu, jq, joff),
+                              (8 * (n + 1) + 8 * n_k2 + 8 * es * n_sel) / n)
     out = {}
     for k, (fn, bpe) in cases.items():
         ms = timed(fn)
         gbs = n * bpe / (ms * 1e-3) / 1e9
         out[k] = {"ms": ms, "events_per_s": n / (ms * 1e-3), "bytes_per_event": bpe, "achieved_GBs": gbs,
                   "frac_of_peak": gbs / peak}
-    del s1, s2
+    out["dimuon_jagged"]["selected_events"] = n_sel
+    out["dimuon_jagged"]["note"] = ("bytes/event = offsets + charges of 2-muon events + kinematics of "
+                                    "selected events (algorithmic)")
+    del s1, s2, jmu, jq, joff
     return out
 
 

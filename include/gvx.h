@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define GVX_ABI_VERSION 1
+#define GVX_ABI_VERSION 2
 
 typedef struct CUstream_st *gvx_stream_t; /* == cudaStream_t */
 
@@ -137,6 +137,25 @@ gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4
                               int32_t nbins, unsigned long long *bins, uint32_t flags,
                               void *m_out, const gvx_vec4_view *boosted_out,
                               gvx_stream_t stream);
+
+/*
+ * gvx_dimuon_histogram — jagged, RDataFrame-style events (PAPER.md:366 names
+ * the RDataFrame integration as the next step; DESIGN.md
+ * R21). Event e owns muons j in [offsets[e], offsets[e+1]) of a flat PtEtaPhiM
+ * collection `muons` (any view) with int32 charges `charge[j]`. The event is
+ * selected iff it has exactly two muons and charge[j0] * charge[j0+1] < 0;
+ * its pair mass (as gvx_invariant_mass) is binned exactly as
+ * gvx_mass_histogram bins (bins accumulate; the caller zeroes them).
+ *   offsets   n_events + 1 int64, non-decreasing, all within the muon arrays
+ *             (caller's guarantee; not re-validated on the device).
+ *   m_out     NULL or n_events masses of dtype: the pair mass, NaN if the event
+ *             is not selected.
+ * The number of selected events is the sum of the bins this call added.
+ */
+gvx_status gvx_dimuon_histogram(gvx_dtype dtype, const gvx_vec4_cview *muons, const int32_t *charge,
+                                const int64_t *offsets, int64_t n_events, double lo, double hi,
+                                int32_t nbins, unsigned long long *bins, void *m_out,
+                                gvx_stream_t stream);
 
 /* Human-readable name of a status code (static storage). */
 const char *gvx_status_string(gvx_status status);

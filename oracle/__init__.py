@@ -59,6 +59,9 @@ def _load():
             getattr(lib, f"gvx_ref_mass_histogram_{sfx}").argtypes = [
                 ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                 ctypes.c_int, P, P]
+            f = getattr(lib, f"gvx_ref_dimuon_histogram_{sfx}")
+            f.argtypes = [P, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P]
+            f.restype = I64
         lib.gvx_ref_find_bin.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_int32]
         lib.gvx_ref_find_bin.restype = ctypes.c_int32
@@ -174,6 +177,27 @@ def mass_histogram(v1, v2, lo: float, hi: float, nbins: int, cm: bool = False,
     getattr(_load(), f"gvx_ref_mass_histogram_{_sfx(v1.dtype)}")(
         _COORDS[coords], _ptr(v1), _ptr(v2), n, lo, hi, nbins, int(bool(cm)), _ptr(bins), _ptr(m))
     return bins, m
+
+
+def dimuon_histogram(muons, charge, offsets, lo: float, hi: float, nbins: int, bins=None):
+    """Jagged dimuon selection + histogram (reading R21): events with exactly two muons of
+    opposite charge. ``muons`` [M, 4] PtEtaPhiM, ``charge`` int32 [M], ``offsets`` int64
+    [n_events + 1]. Returns ``(bins uint64[nbins+2], M_per_event (NaN if not selected), n_selected)``."""
+    muons = _vecs(muons, 4)
+    charge = np.ascontiguousarray(charge, np.int32)
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    if charge.shape != (muons.shape[0],):
+        raise ValueError("charge must have one entry per muon")
+    n_events = offsets.shape[0] - 1
+    if n_events < 0 or (n_events > 0 and (offsets[0] < 0 or offsets[-1] > muons.shape[0] or
+                                          np.any(np.diff(offsets) < 0))):
+        raise ValueError("offsets must be non-decreasing within [0, n_muons]")
+    if bins is None:
+        bins = np.zeros(nbins + 2, np.uint64)
+    m = np.empty(max(n_events, 0), muons.dtype)
+    sel = getattr(_load(), f"gvx_ref_dimuon_histogram_{_sfx(muons.dtype)}")(
+        _ptr(muons), _ptr(charge), _ptr(offsets), max(n_events, 0), lo, hi, nbins, _ptr(bins), _ptr(m))
+    return bins, m, int(sel)
 
 
 def find_bin(x: float, lo: float, hi: float, nbins: int) -> int:

@@ -35,7 +35,10 @@ int32_t gvx_ref_find_bin(double x, double lo, double hi, int32_t nbins);
     void gvx_ref_cm_mass_##SFX(int coords, const T *v1, const T *v2, int64_t n, T *m_out,         \
                                T *elab_out, T *boosted_out);                                      \
     void gvx_ref_mass_histogram_##SFX(int coords, const T *v1, const T *v2, int64_t n, double lo, \
-                                      double hi, int32_t nbins, int cm, uint64_t *bins, T *m_out);
+                                      double hi, int32_t nbins, int cm, uint64_t *bins, T *m_out);  \
+    int64_t gvx_ref_dimuon_histogram_##SFX(const T *muons, const int32_t *charge,                 \
+                                           const int64_t *offsets, int64_t n_events, double lo,   \
+                                           double hi, int32_t nbins, uint64_t *bins, T *m_out);
 
 GVX_REF_DECLARE(float, f32)
 GVX_REF_DECLARE(double, f64)

@@ -43,7 +43,7 @@ GVX_PXPYPZE = 1
 GVX_PXPYPZM = 2
 GVX_PTETAPHIE = 3
 GVX_HIST_BOOST_TO_CM = 0x1
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # The default histogram of the north star: 1000 bins over the dimuon range
 # (reading R13).
@@ -95,6 +95,9 @@ def _load_lib():
                                        ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, ctypes.c_uint32, P,
                                        ctypes.POINTER(Vec4View), P]
     lib.gvx_mass_histogram.restype = st
+    lib.gvx_dimuon_histogram.argtypes = [st, ctypes.POINTER(Vec4CView), P, P, I64, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_int32, P, P, P]
+    lib.gvx_dimuon_histogram.restype = st
     lib.gvx_status_string.argtypes = [st]
     lib.gvx_status_string.restype = ctypes.c_char_p
     lib.gvx_last_cuda_error_string.argtypes = []
@@ -291,6 +294,36 @@ def mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = D
         _check(lib.gvx_mass_histogram(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b), n,
                                       float(lo), float(hi), int(nbins), bins.data_ptr(), flags, mptr, bo_ref,
                                       _stream(dev)), "gvx_mass_histogram")
+    return bins
+
+
+def dimuon_histogram(muons: VecArg, charge: torch.Tensor, offsets: torch.Tensor, lo: float = DEFAULT_LO,
+                     hi: float = DEFAULT_HI, nbins: int = DEFAULT_NBINS, bins: Optional[torch.Tensor] = None,
+                     m_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Jagged events (RDataFrame-style, DESIGN R21): events with exactly two opposite-charge
+    muons; their pair masses are binned into ``bins`` ([nbins+2] int64, accumulated).
+    ``muons`` [M, 4] PtEtaPhiM (or SoA), ``charge`` int32 [M], ``offsets`` int64 [n_events + 1]."""
+    a, m, dt, dev, k1 = _view(muons, 4, "muons")
+    _require_cuda(charge, "charge")
+    _require_cuda(offsets, "offsets")
+    if charge.dtype != torch.int32 or charge.shape != (m,) or not charge.is_contiguous():
+        raise ValueError("charge must be a contiguous int32 tensor with one entry per muon")
+    if offsets.dtype != torch.int64 or offsets.dim() != 1 or not offsets.is_contiguous() or offsets.shape[0] < 1:
+        raise ValueError("offsets must be a contiguous int64 tensor of n_events + 1 entries")
+    n_events = offsets.shape[0] - 1
+    if bins is None:
+        bins = new_bins(nbins, dev)
+    if bins.shape != (nbins + 2,) or bins.dtype != torch.int64 or not bins.is_contiguous():
+        raise ValueError(f"bins must be a contiguous int64 tensor of shape [{nbins + 2}]")
+    mptr = None
+    if m_out is not None:
+        if m_out.shape != (n_events,) or m_out.dtype != dt or not m_out.is_contiguous():
+            raise ValueError("m_out must be a contiguous [n_events] tensor of the muons' dtype")
+        mptr = m_out.data_ptr()
+    with torch.cuda.device(dev):
+        _check(lib.gvx_dimuon_histogram(_dtype_code(dt), ctypes.byref(a), charge.data_ptr(), offsets.data_ptr(),
+                                        n_events, float(lo), float(hi), int(nbins), bins.data_ptr(), mptr,
+                                        _stream(dev)), "gvx_dimuon_histogram")
     return bins
 
 

@@ -402,6 +402,28 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
   return launch_hist<T, C, L_GEN, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
 }
 
+// ---------------------------------------------------------- dimuon -------
+template <typename T>
+gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
+                         const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
+  const char* b = (const char*)mu->c[0];
+  bool aos = mu->stride == 4 && aligned(b, 4 * sizeof(T));
+  for (int k = 1; k < 4; ++k) aos = aos && (const char*)mu->c[k] == b + k * sizeof(T);
+  const size_t nb2 = (size_t)hp.nbins + 2;
+  if (nb2 > kMaxSmemBins) return GVX_ERR_UNSUPPORTED;
+  const size_t sm = nb2 * sizeof(unsigned int);
+  auto k = aos ? k_dimuon_histogram<T, true> : k_dimuon_histogram<T, false>;
+  int grid = grid_for(k, kBlock, sm, kBlock, n_events);
+  // uint32 shared-memory bins: one launch covers at most grid * 2^31 events
+  const int64_t chunk = (int64_t)grid << 31;
+  for (int64_t o = 0; o < n_events; o += chunk) {
+    int64_t cn = n_events - o < chunk ? n_events - o : chunk;
+    k<<<grid, kBlock, sm, s>>>(mk4<T>(mu), q, off + o, cn, hp, bins, m_out ? (T*)m_out + o : nullptr);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
 }  // namespace
 
 extern "C" {
@@ -420,6 +442,23 @@ const char* gvx_status_string(gvx_status st) {
 }
 
 const char* gvx_last_cuda_error_string(void) { return g_last_cuda_error.c_str(); }
+
+gvx_status gvx_dimuon_histogram(gvx_dtype dtype, const gvx_vec4_cview* muons, const int32_t* charge,
+                                const int64_t* offsets, int64_t n_events, double lo, double hi, int32_t nbins,
+                                unsigned long long* bins, void* m_out, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || n_events < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
+  if (n_events == 0) return GVX_OK;
+  const size_t es = dsize(dtype);
+  if (!view_ok<4>(muons, es) || !charge || !aligned(charge, 4) || !offsets || !aligned(offsets, 8) || !bins ||
+      !aligned(bins, 8))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if (m_out && !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  HistParams hp{lo, hi, hi - lo, 1.0 / (hi - lo), (double)nbins, nbins};
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GVX_F64) return launch_dimuon<double>(muons, charge, offsets, n_events, hp, bins, m_out, s);
+  return launch_dimuon<float>(muons, charge, offsets, n_events, hp, bins, m_out, s);
+}
 
 gvx_status gvx_invariant_mass(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1, const gvx_vec4_cview* v2,
                               void* m_out, int64_t n, gvx_stream_t stream) {

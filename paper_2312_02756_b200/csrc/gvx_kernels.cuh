@@ -279,6 +279,57 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
 }
 
 // ============================================================================
+// Jagged dimuon selection + mass histogram (DESIGN R21):
+// event e owns muons [offsets[e], offsets[e+1]); selected iff exactly two
+// muons of opposite charge; the pair mass is binned (shared-memory bins).
+// One thread per event, grid-stride: the offsets reads are coalesced, the
+// muon reads of consecutive events are contiguous (256-bit AoS loads).
+// ============================================================================
+template <typename T, bool AOS>
+__global__ void __launch_bounds__(256) k_dimuon_histogram(View4<T> mu, const int32_t* __restrict__ q,
+                                                          const int64_t* __restrict__ offsets, int64_t n_events,
+                                                          HistParams hp, unsigned long long* __restrict__ bins,
+                                                          T* __restrict__ m_out) {
+  extern __shared__ unsigned int shd[];
+  const int nb2 = hp.nbins + 2;
+  for (int b = threadIdx.x; b < nb2; b += blockDim.x) shd[b] = 0u;
+  __syncthreads();
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_events; e += nthr) {
+    const int64_t o = __ldg(offsets + e), k = __ldg(offsets + e + 1) - o;
+    T M = T(NAN);
+    if (k == 2 && __ldg(q + o) * __ldg(q + o + 1) < 0) {
+      T a[4], b[4];
+      if constexpr (AOS) {
+        if constexpr (sizeof(T) == 8) {
+          double ra[4], rb[4];
+          ld256(reinterpret_cast<const double*>(mu.c[0]) + 4 * o, ra);
+          ld256(reinterpret_cast<const double*>(mu.c[0]) + 4 * (o + 1), rb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) { a[c] = (T)ra[c]; b[c] = (T)rb[c]; }
+        } else {
+          float4 ra = __ldg(reinterpret_cast<const float4*>(mu.c[0]) + o);
+          float4 rb = __ldg(reinterpret_cast<const float4*>(mu.c[0]) + o + 1);
+          a[0] = ra.x; a[1] = ra.y; a[2] = ra.z; a[3] = ra.w;
+          b[0] = rb.x; b[1] = rb.y; b[2] = rb.z; b[3] = rb.w;
+        }
+      } else {
+        load_event(mu, o, a);
+        load_event(mu, o + 1, b);
+      }
+      M = event_mass<T, C_PTETAPHIM>(a, b);
+      atomicAdd(&shd[find_bin((double)M, hp)], 1u);
+    }
+    if (m_out) m_out[e] = M;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
+    unsigned int c = shd[b];
+    if (c) atomicAdd(&bins[b], (unsigned long long)c);
+  }
+}
+
+// ============================================================================
 // K1 / K3 on AoS pairs, TMA-fed (the fast path for the paper's LVector* layout).
 //
 // One CTA = 1 producer warp + NCW consumer warps, persistent over tiles of
@@ -406,7 +457,18 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
           lds_vec(src + TV, e, lane, b[u]);
         }
       }
+#if defined(GVX_TUNE) && defined(GVX_RELEASE_BY_DEPENDENCY)
+      {  // tuning experiment only: order the release after the loads by a data dependency
+        uint32_t d = 0;
+#pragma unroll
+        for (int u = 0; u < CFG::EPT; ++u)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) d ^= __float_as_uint((float)a[u][c]) ^ __float_as_uint((float)b[u][c]);
+        if (__any_sync(0xffffffffu, d == 0x7f7f7f7fu)) asm volatile("" ::: "memory");
+      }
+#else
       tma::fence_proxy_async_smem();  // this stage's LDS are performed before its release
+#endif
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
 #pragma unroll

@@ -46,6 +46,11 @@ STREAM_V1 = 1
 STREAM_V2 = 2
 STREAM_BOOST_P = 3
 STREAM_BOOST_BETA = 4
+STREAM_JAGGED_N = 5     # per-event muon multiplicity
+STREAM_JAGGED_MU = 6    # muon j of event e: counter e * 8 + j (j < 8)
+JAGGED_SLOTS = 8
+# multiplicity k = 0..4 with P = 0.25, 0.30, 0.30, 0.10, 0.05 (cumulative thresholds)
+JAGGED_CDF = (0.25, 0.55, 0.85, 0.95)
 
 DEFAULT_SEED = 12345
 
@@ -155,6 +160,33 @@ def boost_inputs(idx, seed=DEFAULT_SEED, dtype=np.float64):
     v = np.stack([px, py, pz, e], axis=1).astype(dtype)
     beta = np.stack([gx * scale, gy * scale, gz * scale], axis=1).astype(dtype)
     return v, beta
+
+
+def jagged_counts(event_idx, seed=DEFAULT_SEED):
+    """Muon multiplicity of each event (0..4), from one uniform per event."""
+    idx = np.asarray(event_idx, np.uint64).reshape(-1)
+    u = _u(_draw(idx, 0, STREAM_JAGGED_N, seed)[0])
+    k = np.zeros(idx.size, np.int64)
+    for t in JAGGED_CDF:
+        k += (u >= t)
+    return k
+
+
+def jagged_events(first_event: int, n_events: int, seed=DEFAULT_SEED, dtype=np.float64):
+    """A flat, RDataFrame-style muon collection for events first_event .. first_event+n_events-1:
+    ``(muons [M, 4] PtEtaPhiM, charge int32 [M], offsets int64 [n_events + 1])``. Muon j of
+    event e is drawn from counter e * 8 + j, charge = +1 / -1 with probability 1/2, so any
+    shard of events regenerates identically."""
+    ev = np.arange(first_event, first_event + n_events, dtype=np.uint64)
+    k = jagged_counts(ev, seed)
+    offsets = np.zeros(n_events + 1, np.int64)
+    np.cumsum(k, out=offsets[1:])
+    ev_of = np.repeat(ev, k)
+    j = np.arange(offsets[-1], dtype=np.int64) - np.repeat(offsets[:-1], k)
+    midx = ev_of * np.uint64(JAGGED_SLOTS) + j.astype(np.uint64)
+    mu = muons(midx, STREAM_JAGGED_MU, seed, dtype)
+    q = np.where(_u(_draw(midx, 2, STREAM_JAGGED_MU, seed)[0]) < 0.5, 1, -1).astype(np.int32)
+    return mu, q, offsets
 
 
 def shard_range(n_total: int, rank: int, world: int):

@@ -24,6 +24,12 @@ def _load():
             f.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
                           ctypes.c_void_p, ctypes.c_void_p]
             f.restype = ctypes.c_int
+        lib.gvx_synth_jagged_counts.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
+                                                ctypes.c_void_p]
+        lib.gvx_synth_jagged_counts.restype = ctypes.c_int
+        lib.gvx_synth_jagged_fill.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.gvx_synth_jagged_fill.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -62,3 +68,24 @@ def boost_inputs(n: int, first: int = 0, seed: int = DEFAULT_SEED, dtype=torch.f
     if rc:
         raise RuntimeError(f"gvx_synth_boost_inputs: cuda error {rc}")
     return v, beta
+
+
+def jagged_events(first_event: int, n_events: int, seed: int = DEFAULT_SEED, dtype=torch.float64, device="cuda"):
+    """Device twin of synth.jagged_events: (muons [M, 4], charge int32 [M], offsets int64 [n+1])."""
+    dev = torch.device(device)
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev).cuda_stream
+        counts = torch.empty(n_events, dtype=torch.int64, device=dev)
+        rc = _load().gvx_synth_jagged_counts(seed, first_event, n_events, counts.data_ptr(), st)
+        if rc:
+            raise RuntimeError(f"gvx_synth_jagged_counts: cuda error {rc}")
+        offsets = torch.zeros(n_events + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(counts, 0, out=offsets[1:])
+        m = int(offsets[-1].item())
+        mu = torch.empty((m, 4), dtype=dtype, device=dev)
+        q = torch.empty(m, dtype=torch.int32, device=dev)
+        rc = _load().gvx_synth_jagged_fill(_code(dtype), seed, first_event, n_events, offsets.data_ptr(),
+                                           mu.data_ptr(), q.data_ptr(), st)
+        if rc:
+            raise RuntimeError(f"gvx_synth_jagged_fill: cuda error {rc}")
+    return mu, q, offsets

@@ -12,6 +12,7 @@ namespace {
 
 constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
 constexpr uint32_t STREAM_V1 = 1, STREAM_V2 = 2, STREAM_BOOST_P = 3, STREAM_BOOST_BETA = 4;
+constexpr uint32_t STREAM_JAGGED_N = 5, STREAM_JAGGED_MU = 6, JAGGED_SLOTS = 8;
 
 __device__ __forceinline__ uint4 philox(uint64_t idx, uint32_t call, uint32_t stream, uint64_t seed) {
   uint32_t c0 = (uint32_t)idx, c1 = (uint32_t)(idx >> 32), c2 = call, c3 = stream;
@@ -97,6 +98,25 @@ __global__ void k_boost_inputs(uint64_t seed, uint64_t first, int64_t n, T* v, T
   }
 }
 
+__global__ void k_jagged_counts(uint64_t seed, uint64_t first, int64_t n, int64_t* counts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double u = u01(philox(first + (uint64_t)i, 0, STREAM_JAGGED_N, seed).x);
+    counts[i] = (int64_t)(u >= 0.25) + (int64_t)(u >= 0.55) + (int64_t)(u >= 0.85) + (int64_t)(u >= 0.95);
+  }
+}
+
+template <typename T>
+__global__ void k_jagged_fill(uint64_t seed, uint64_t first, int64_t n, const int64_t* offsets, T* mu, int32_t* q) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = offsets[i], k = offsets[i + 1] - o;
+    for (int64_t j = 0; j < k; ++j) {
+      uint64_t idx = (first + (uint64_t)i) * JAGGED_SLOTS + (uint64_t)j;
+      muon<T>(idx, STREAM_JAGGED_MU, seed, mu + 4 * (o + j));
+      q[o + j] = u01(philox(idx, 2, STREAM_JAGGED_MU, seed).x) < 0.5 ? 1 : -1;
+    }
+  }
+}
+
 int grid_of(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
@@ -121,6 +141,25 @@ int gvx_synth_boost_inputs(int dtype, uint64_t seed, uint64_t first, int64_t n, 
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == 1) k_boost_inputs<double><<<grid_of(n), 256, 0, s>>>(seed, first, n, (double*)v, (double*)beta);
   else k_boost_inputs<float><<<grid_of(n), 256, 0, s>>>(seed, first, n, (float*)v, (float*)beta);
+  return (int)cudaGetLastError();
+}
+
+// Jagged events: per-event multiplicities (int64 [n]), then, given the
+// exclusive prefix sum offsets [n+1] (relative to the shard), the muons
+// (AoS [M][4]) and charges (int32 [M]).
+int gvx_synth_jagged_counts(uint64_t seed, uint64_t first, int64_t n, void* counts, void* stream) {
+  if (n <= 0) return 0;
+  k_jagged_counts<<<grid_of(n), 256, 0, (cudaStream_t)stream>>>(seed, first, n, (int64_t*)counts);
+  return (int)cudaGetLastError();
+}
+int gvx_synth_jagged_fill(int dtype, uint64_t seed, uint64_t first, int64_t n, const void* offsets, void* mu,
+                          void* q, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == 1)
+    k_jagged_fill<double><<<grid_of(n), 256, 0, s>>>(seed, first, n, (const int64_t*)offsets, (double*)mu, (int32_t*)q);
+  else
+    k_jagged_fill<float><<<grid_of(n), 256, 0, s>>>(seed, first, n, (const int64_t*)offsets, (float*)mu, (int32_t*)q);
   return (int)cudaGetLastError();
 }
 

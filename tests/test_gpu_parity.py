@@ -494,3 +494,28 @@ def test_other_coordinate_systems(gvx, O, dt, coords):
         nanp = (np.isnan(mho) | (np.abs(mlab.astype(np.float64)) < (1e-2 if dt == np.float32 else 1e-6) * e)) if cm else None
         fails, _ = hist_check(h, mho, e, tau, LO, HI, NB, nan_possible=nanp, m_window_center=mlab if cm else None)
         assert not fails, (cm, fails)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_dimuon_histogram_parity(gvx, O, dt):
+    mu, q, off = synth.jagged_events(0, 400_003, seed=8, dtype=dt)
+    bins_o, mo, sel = O.dimuon_histogram(mu, q, off, LO, HI, NB)
+    tm, tq, to = dev(mu), dev(q), dev(off)
+    m_out = torch.empty(off.size - 1, dtype=TDT[dt], device="cuda")
+    h = host(gvx.dimuon_histogram(tm, tq, to, m_out=m_out))
+    mg = host(m_out)
+    assert int(h.sum()) == sel
+    assert np.array_equal(np.isnan(mg), np.isnan(mo))
+    ok = ~np.isnan(mo)
+    # tolerance scale: the selected pair's E_lab from the oracle
+    first = off[:-1][ok]
+    _, e = O.invariant_mass(mu[first], mu[first + 1])
+    assert mass_violations(mg[ok], mo[ok], e, tau_of(dt)).size == 0
+    fails, _ = hist_check(h, mo[ok], e, tau_of(dt), LO, HI, NB)
+    assert not fails, fails
+    # SoA view of the muons gives the same bits; the device generator twin gives the same events
+    hs = host(gvx.dimuon_histogram([tm[:, k].contiguous() for k in range(4)], tq, to))
+    assert np.array_equal(hs, h)
+    import synth.device as sd
+    dmu, dq, doff = sd.jagged_events(0, off.size - 1, seed=8, dtype=TDT[dt])
+    assert torch.equal(dmu, tm) and torch.equal(dq, tq) and torch.equal(doff, to)

@@ -472,3 +472,47 @@ def test_ptetaphie_single_vector_mpmath(O):
         pt, eta, E = (mp.mpf(float(x)) for x in (v[i, 0], v[i, 1], v[i, 3]))
         M2 = E * E - (pt * mp.cosh(eta)) ** 2
         assert abs(mp.mpf(float(m[i])) ** 2 - M2) <= 1e-14 * E * E
+
+
+# --------------------------------------------------------------------------
+# Jagged dimuon selection (reading R21)
+# --------------------------------------------------------------------------
+
+def test_dimuon_selection_brute_force(O):
+    mu, q, off = synth.jagged_events(0, 20_000, seed=3)
+    bins, m, sel = O.dimuon_histogram(mu, q, off, 0.25, 300.0, 1000)
+    k = np.diff(off)
+    expect_sel = 0
+    ref = np.zeros(1002, np.uint64)
+    for e in range(off.size - 1):
+        a, b = off[e], off[e + 1]
+        if b - a == 2 and q[a] != q[a + 1]:  # exactly two, opposite charge (q = ±1)
+            expect_sel += 1
+            mm, _ = O.invariant_mass(mu[a:a + 1], mu[a + 1:a + 2])
+            assert m[e] == mm[0]
+            ref[O.find_bin(float(mm[0]), 0.25, 300.0, 1000)] += 1
+        else:
+            assert np.isnan(m[e])
+    assert sel == expect_sel == int(bins.sum())
+    assert np.array_equal(bins, ref)
+    # the multiplicity / charge recipe: P(k = 2) = 0.30, opposite charges half of those
+    assert abs((k == 2).mean() - 0.30) < 0.01
+    assert abs(sel / off.size - 0.15) < 0.01
+
+
+def test_dimuon_closed_forms(O):
+    m_mu = synth.MUON_MASS
+    mu = np.array([[45, 0.3, 0.1, m_mu], [40, -0.8, 2.9, m_mu],     # event 0: opposite -> selected
+                   [45, 0.3, 0.1, m_mu], [40, -0.8, 2.9, m_mu],     # event 1: same sign -> rejected
+                   [25, 1.1, 0.3, 0], [25, -1.1, 0.3 - np.pi, 0],   # event 2: back-to-back massless
+                   [10, 0, 0, m_mu], [10, 0, 1, m_mu], [10, 0, 2, m_mu]])  # event 3: three muons -> rejected
+    q = np.array([1, -1, -1, -1, 1, -1, 1, -1, 1], np.int32)
+    off = np.array([0, 2, 4, 6, 9, 9])  # event 4: empty
+    bins, m, sel = O.dimuon_histogram(mu, q, off, 0.25, 300.0, 1000)
+    assert sel == 2
+    assert m[0] == pytest.approx(96.946954876884514685, rel=1e-14)
+    assert m[2] == pytest.approx(2 * 25 * np.cosh(1.1), rel=1e-12)
+    assert np.isnan(m[1]) and np.isnan(m[3]) and np.isnan(m[4])
+    # no events
+    bins, m, sel = O.dimuon_histogram(np.zeros((0, 4)), np.zeros(0, np.int32), np.zeros(1, np.int64), 0.25, 300.0, 1000)
+    assert sel == 0 and m.size == 0
