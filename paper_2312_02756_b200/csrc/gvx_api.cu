@@ -413,7 +413,7 @@ gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64
   if (nb2 > kMaxSmemBins) return GVX_ERR_UNSUPPORTED;
   const size_t sm = nb2 * sizeof(unsigned int);
   auto k = aos ? k_dimuon_histogram<T, true> : k_dimuon_histogram<T, false>;
-  int grid = grid_for(k, kBlock, sm, kBlock, n_events);
+  int grid = grid_for(k, kBlock, sm, kBlock * 4, n_events);
   // uint32 shared-memory bins: one launch covers at most grid * 2^31 events
   const int64_t chunk = (int64_t)grid << 31;
   for (int64_t o = 0; o < n_events; o += chunk) {

@@ -286,6 +286,26 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
 // muon reads of consecutive events are contiguous (256-bit AoS loads).
 // ============================================================================
 template <typename T, bool AOS>
+__device__ __forceinline__ void load_muon(const View4<T>& mu, int64_t j, T (&x)[4]) {
+  if constexpr (AOS) {
+    if constexpr (sizeof(T) == 8) {
+      double r[4];
+      ld256(reinterpret_cast<const double*>(mu.c[0]) + 4 * j, r);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) x[c] = (T)r[c];
+    } else {
+      float4 r = __ldg(reinterpret_cast<const float4*>(mu.c[0]) + j);
+      x[0] = r.x; x[1] = r.y; x[2] = r.z; x[3] = r.w;
+    }
+  } else {
+    load_event(mu, j, x);
+  }
+}
+
+// U events per thread per iteration, loads batched stage by stage (offsets,
+// then charges, then kinematics) so U independent dependency chains are in
+// flight per thread instead of one.
+template <typename T, bool AOS, int U = 4>
 __global__ void __launch_bounds__(256) k_dimuon_histogram(View4<T> mu, const int32_t* __restrict__ q,
                                                           const int64_t* __restrict__ offsets, int64_t n_events,
                                                           HistParams hp, unsigned long long* __restrict__ bins,
@@ -295,32 +315,39 @@ __global__ void __launch_bounds__(256) k_dimuon_histogram(View4<T> mu, const int
   for (int b = threadIdx.x; b < nb2; b += blockDim.x) shd[b] = 0u;
   __syncthreads();
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_events; e += nthr) {
-    const int64_t o = __ldg(offsets + e), k = __ldg(offsets + e + 1) - o;
-    T M = T(NAN);
-    if (k == 2 && __ldg(q + o) * __ldg(q + o + 1) < 0) {
-      T a[4], b[4];
-      if constexpr (AOS) {
-        if constexpr (sizeof(T) == 8) {
-          double ra[4], rb[4];
-          ld256(reinterpret_cast<const double*>(mu.c[0]) + 4 * o, ra);
-          ld256(reinterpret_cast<const double*>(mu.c[0]) + 4 * (o + 1), rb);
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n_events; e0 += nthr * U) {
+    int64_t o[U];
+    bool two[U], sel[U];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) { a[c] = (T)ra[c]; b[c] = (T)rb[c]; }
-        } else {
-          float4 ra = __ldg(reinterpret_cast<const float4*>(mu.c[0]) + o);
-          float4 rb = __ldg(reinterpret_cast<const float4*>(mu.c[0]) + o + 1);
-          a[0] = ra.x; a[1] = ra.y; a[2] = ra.z; a[3] = ra.w;
-          b[0] = rb.x; b[1] = rb.y; b[2] = rb.z; b[3] = rb.w;
-        }
-      } else {
-        load_event(mu, o, a);
-        load_event(mu, o + 1, b);
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * nthr;
+      two[u] = false;
+      o[u] = 0;
+      if (e < n_events) {
+        o[u] = __ldg(offsets + e);
+        two[u] = __ldg(offsets + e + 1) - o[u] == 2;
       }
-      M = event_mass<T, C_PTETAPHIM>(a, b);
-      atomicAdd(&shd[find_bin((double)M, hp)], 1u);
     }
-    if (m_out) m_out[e] = M;
+#pragma unroll
+    for (int u = 0; u < U; ++u) sel[u] = two[u] && __ldg(q + o[u]) * __ldg(q + o[u] + 1) < 0;
+    T a[U][4], b[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (sel[u]) {
+        load_muon<T, AOS>(mu, o[u], a[u]);
+        load_muon<T, AOS>(mu, o[u] + 1, b[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * nthr;
+      if (e >= n_events) break;
+      T M = T(NAN);
+      if (sel[u]) {
+        M = event_mass<T, C_PTETAPHIM>(a[u], b[u]);
+        atomicAdd(&shd[find_bin((double)M, hp)], 1u);
+      }
+      if (m_out) m_out[e] = M;
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
