@@ -38,6 +38,9 @@ BYTES = {
     "mass_histogram_cm": lambda es: 8 * es,
 }
 KERNEL_ORDER = ["invariant_mass", "boost", "mass_histogram", "mass_histogram_cm"]
+# Λ(β = (0, 0, 0.6)) · R_z(0.7): a general Lorentz transformation for the --extended timing
+_c, _s, _g = 0.7648421872844885, 0.644217687237691, 1.25
+LORENTZ_DEMO = [[_c, -_s, 0, 0], [_s, _c, 0, 0], [0, 0, _g, _g * 0.6], [0, 0, _g * 0.6, _g]]
 
 
 def parse():
@@ -384,6 +387,7 @@ def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
         "mass_soa": (lambda: gvx.invariant_mass(s1, s2, out=m), 9 * es),
         "hist_soa": (lambda: gvx.mass_histogram(s1, s2), 8 * es),
         "boost_uniform": (lambda: gvx.boost_uniform(bv, (0.3, -0.4, 0.5), out=bout), 8 * es),
+        "lorentz_4x4": (lambda: gvx.lorentz_transform(bv, LORENTZ_DEMO, out=bout), 8 * es),
     }
     # jagged events (f4): 1 event per pair slot of the batch, ~1.1 muons/event on average
     import synth.device as sd

@@ -119,6 +119,18 @@ gvx_status gvx_boost_uniform(gvx_dtype dtype, const gvx_vec4_cview *v, double bx
                              gvx_stream_t stream);
 
 /*
+ * gvx_lorentz_transform — ApplyBoost with a general Lorentz transformation
+ * "represented internally by a 4x4 orthosymplectic matrix" (
+ * SURVEY §8(f) f2): out[i] = L * v[i], PxPyPzE in and out.
+ *   L     16 doubles, row-major, HOST pointer (copied at the call; rounded to
+ *         dtype). Must satisfy L^T g L = g, g = diag(-1,-1,-1,+1), to 1e-9
+ *         relative, and be finite, else GVX_ERR_DOMAIN (nothing enqueued).
+ *   v, out  n vectors (device); out may equal v exactly (in place).
+ */
+gvx_status gvx_lorentz_transform(gvx_dtype dtype, const gvx_vec4_cview *v, const double *L,
+                                 const gvx_vec4_view *out, int64_t n, gvx_stream_t stream);
+
+/*
  * gvx_mass_histogram — fused InvariantMass + histogram (north_star;
  * BASELINE.json configs[3], configs[4]). For each pair the signed mass M (as
  * gvx_invariant_mass; with flags & GVX_HIST_BOOST_TO_CM, the mass after

@@ -55,6 +55,9 @@ def _load():
             f = getattr(lib, f"gvx_ref_boost_uniform_{sfx}")
             f.argtypes = [P, T, T, T, I64, P]
             f.restype = ctypes.c_int
+            f = getattr(lib, f"gvx_ref_lorentz_transform_{sfx}")
+            f.argtypes = [P, P, I64, P]
+            f.restype = ctypes.c_int
             getattr(lib, f"gvx_ref_cm_mass_{sfx}").argtypes = [ctypes.c_int, P, P, I64, P, P, P]
             getattr(lib, f"gvx_ref_mass_histogram_{sfx}").argtypes = [
                 ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
@@ -139,6 +142,18 @@ def boost_uniform(v, bx, by, bz):
     rc = getattr(_load(), f"gvx_ref_boost_uniform_{_sfx(v.dtype)}")(_ptr(v), bx, by, bz, n, _ptr(out))
     if rc != 0:
         raise DomainError(f"|beta|^2 = {bx*bx + by*by + bz*bz} >= 1")
+    return out
+
+
+def lorentz_transform(v, L):
+    """General 4x4 Lorentz transformation ("orthosymplectic matrix"): out = L·v.
+    ``L`` 4x4 (row-major, double); raises DomainError unless L^T g L = g (to 1e-9)."""
+    v = _vecs(v, 4)
+    Lm = np.ascontiguousarray(L, np.float64).reshape(4, 4)
+    out = np.empty_like(v)
+    rc = getattr(_load(), f"gvx_ref_lorentz_transform_{_sfx(v.dtype)}")(_ptr(Lm), _ptr(v), v.shape[0], _ptr(out))
+    if rc != 0:
+        raise DomainError("L is not a Lorentz transformation (L^T g L != g)")
     return out
 
 

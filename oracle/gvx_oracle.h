@@ -32,6 +32,7 @@ int32_t gvx_ref_find_bin(double x, double lo, double hi, int32_t nbins);
                                       T *elab_out);                                               \
     void gvx_ref_boost_##SFX(const T *v, const T *beta, int64_t n, T *out, T *scale_out);         \
     int gvx_ref_boost_uniform_##SFX(const T *v, T bx, T by, T bz, int64_t n, T *out);             \
+    int gvx_ref_lorentz_transform_##SFX(const double *L, const T *v, int64_t n, T *out);          \
     void gvx_ref_cm_mass_##SFX(int coords, const T *v1, const T *v2, int64_t n, T *m_out,         \
                                T *elab_out, T *boosted_out);                                      \
     void gvx_ref_mass_histogram_##SFX(int coords, const T *v1, const T *v2, int64_t n, double lo, \

@@ -95,6 +95,8 @@ def _load_lib():
                                        ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, ctypes.c_uint32, P,
                                        ctypes.POINTER(Vec4View), P]
     lib.gvx_mass_histogram.restype = st
+    lib.gvx_lorentz_transform.argtypes = [st, ctypes.POINTER(Vec4CView), P, ctypes.POINTER(Vec4View), I64, P]
+    lib.gvx_lorentz_transform.restype = st
     lib.gvx_dimuon_histogram.argtypes = [st, ctypes.POINTER(Vec4CView), P, P, I64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_int32, P, P, P]
     lib.gvx_dimuon_histogram.restype = st
@@ -249,6 +251,19 @@ def boost_uniform(v: VecArg, beta: Sequence[float], out: Optional[VecArg] = None
     with torch.cuda.device(dev):
         _check(lib.gvx_boost_uniform(_dtype_code(dt), ctypes.byref(a), bx, by, bz, ctypes.byref(o), n,
                                      _stream(dev)), "gvx_boost_uniform")
+    return out
+
+
+def lorentz_transform(v: VecArg, L, out: Optional[VecArg] = None) -> VecArg:
+    """ApplyBoost with a general 4x4 Lorentz matrix: ``out[i] = L @ v[i]``.
+    ``L`` is any 4x4 array-like (row-major); non-Lorentz L raises :class:`DomainError`."""
+    import numpy as _np
+    Lm = _np.ascontiguousarray(_np.asarray(L, dtype=_np.float64).reshape(4, 4))
+    a, n, dt, dev, k1 = _view(v, 4, "v")
+    out, o = _boost_out(v, n, dt, dev, out)
+    with torch.cuda.device(dev):
+        _check(lib.gvx_lorentz_transform(_dtype_code(dt), ctypes.byref(a), Lm.ctypes.data, ctypes.byref(o), n,
+                                         _stream(dev)), "gvx_lorentz_transform")
     return out
 
 

@@ -402,6 +402,47 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
   return launch_hist<T, C, L_GEN, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
 }
 
+// ---------------------------------------------------------- lorentz ------
+template <typename T>
+gvx_status launch_lorentz(const gvx_vec4_cview* v, const double* Lrm, const gvx_vec4_view* out, int64_t n,
+                          cudaStream_t s) {
+  Mat4<T> L;
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) L.m[r][c] = (T)Lrm[4 * r + c];
+  const char* vb = (const char*)v->c[0];
+  const char* ob = (const char*)out->c[0];
+  bool aos = v->stride == 4 && out->stride == 4 && aligned(vb, 4 * sizeof(T)) && aligned(ob, 4 * sizeof(T));
+  for (int k = 1; k < 4; ++k)
+    aos = aos && (const char*)v->c[k] == vb + k * sizeof(T) && (const char*)out->c[k] == ob + k * sizeof(T);
+  if (aos) {
+    auto k = k_lorentz<T, true>;
+    k<<<grid_for(k, kBlock, 0, kBlock, n), kBlock, 0, s>>>(mk4<T>(v), mk4o<T>(out), n, L);
+  } else {
+    auto k = k_lorentz<T, false>;
+    k<<<grid_for(k, kBlock, 0, kBlock, n), kBlock, 0, s>>>(mk4<T>(v), mk4o<T>(out), n, L);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+// L^T g L = g within 1e-9 max(1, |L|^2), g = diag(-1,-1,-1,+1); all entries finite.
+bool is_lorentz(const double* L) {
+  static const double g[4] = {-1, -1, -1, 1};
+  double lmax = 0;
+  for (int k = 0; k < 16; ++k) {
+    if (!isfinite(L[k])) return false;
+    lmax = fabs(L[k]) > lmax ? fabs(L[k]) : lmax;
+  }
+  const double tol = 1e-9 * (lmax * lmax > 1 ? lmax * lmax : 1);
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) {
+      double m = 0;
+      for (int r = 0; r < 4; ++r) m += L[4 * r + a] * g[r] * L[4 * r + b];
+      if (fabs(m - (a == b ? g[a] : 0.0)) > tol) return false;
+    }
+  return true;
+}
+
 // ---------------------------------------------------------- dimuon -------
 template <typename T>
 gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
@@ -442,6 +483,18 @@ const char* gvx_status_string(gvx_status st) {
 }
 
 const char* gvx_last_cuda_error_string(void) { return g_last_cuda_error.c_str(); }
+
+gvx_status gvx_lorentz_transform(gvx_dtype dtype, const gvx_vec4_cview* v, const double* L,
+                                 const gvx_vec4_view* out, int64_t n, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || n < 0 || !L) return GVX_ERR_INVALID_ARGUMENT;
+  if (!is_lorentz(L)) return GVX_ERR_DOMAIN;
+  if (n == 0) return GVX_OK;
+  const size_t es = dsize(dtype);
+  if (!view_ok<4>(v, es) || !out_view_ok(out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GVX_F64) return launch_lorentz<double>(v, L, out, n, s);
+  return launch_lorentz<float>(v, L, out, n, s);
+}
 
 gvx_status gvx_dimuon_histogram(gvx_dtype dtype, const gvx_vec4_cview* muons, const int32_t* charge,
                                 const int64_t* offsets, int64_t n_events, double lo, double hi, int32_t nbins,

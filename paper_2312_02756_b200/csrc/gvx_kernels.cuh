@@ -199,6 +199,52 @@ __global__ void __launch_bounds__(256) k_boost(View4<T> v, View3<T> beta, View4o
 }
 
 // ============================================================================
+// General 4x4 Lorentz transformation ("4x4 orthosymplectic
+// matrix"): out = L v, L uniform (kernel parameter).
+// ============================================================================
+template <typename T> struct Mat4 { T m[4][4]; };
+
+template <typename T, bool AOS>
+__global__ void __launch_bounds__(256) k_lorentz(View4<T> v, View4o<T> out, int64_t n, Mat4<T> L) {
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthr) {
+    T x[4];
+    if constexpr (AOS) {
+      if constexpr (sizeof(T) == 8) {
+        double r[4];
+        ld256(reinterpret_cast<const double*>(v.c[0]) + 4 * i, r);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) x[c] = (T)r[c];
+      } else {
+        float4 r = __ldcs(reinterpret_cast<const float4*>(v.c[0]) + i);
+        x[0] = r.x; x[1] = r.y; x[2] = r.z; x[3] = r.w;
+      }
+    } else {
+      load_event(v, i, x);
+    }
+    T o[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      T acc = L.m[r][0] * x[0];
+#pragma unroll
+      for (int c = 1; c < 4; ++c) acc = fma(L.m[r][c], x[c], acc);
+      o[r] = acc;
+    }
+    if constexpr (AOS) {
+      if constexpr (sizeof(T) == 8) {
+        double r[4] = {(double)o[0], (double)o[1], (double)o[2], (double)o[3]};
+        st256(reinterpret_cast<double*>(out.c[0]) + 4 * i, r);
+      } else {
+        __stcs(reinterpret_cast<float4*>(out.c[0]) + i, make_float4(o[0], o[1], o[2], o[3]));
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) out.c[c][i * out.s] = o[c];
+    }
+  }
+}
+
+// ============================================================================
 // K3: fused mass (lab or CM frame) + histogram, privatised in shared memory.
 // ============================================================================
 template <typename T, int COORDS, bool CM, bool WANT_BO = false>

@@ -80,6 +80,28 @@ def test_validation_codes(gvx):
     assert H(gvx.GVX_F64, 0, by(a), by(b), 0, 0.0, 1.0, 10, None, 0, None, None, None) == 0
 
 
+def test_lorentz_matrix_validation(gvx):
+    """gvx_lorentz_transform checks L^T g L = g on the host before anything is enqueued."""
+    L = gvx.lib
+    by = ctypes.byref
+    a, o = _view(), gvx.Vec4View()
+    for k in range(4):
+        o.c[k] = 0x3000 + 8 * k
+    o.stride = 4
+    D = ctypes.c_double * 16
+    eye = D(*[1.0 if i % 5 == 0 else 0.0 for i in range(16)])
+    two = D(*[2.0 if i % 5 == 0 else 0.0 for i in range(16)])
+    nan = D(*[float("nan")] * 16)
+    import math
+    g, b = 1 / math.sqrt(1 - 0.36), 0.6
+    boost_z = D(1, 0, 0, 0, 0, 1, 0, 0, 0, 0, g, g * b, 0, 0, g * b, g)
+    assert L.gvx_lorentz_transform(gvx.GVX_F64, by(a), eye, by(o), 0, None) == 0
+    assert L.gvx_lorentz_transform(gvx.GVX_F64, by(a), boost_z, by(o), 0, None) == 0
+    assert L.gvx_lorentz_transform(gvx.GVX_F64, by(a), two, by(o), 4, None) == 2
+    assert L.gvx_lorentz_transform(gvx.GVX_F32, by(a), nan, by(o), 4, None) == 2
+    assert L.gvx_lorentz_transform(gvx.GVX_F64, by(a), None, by(o), 4, None) == 1
+
+
 def test_python_binding_rejects_cpu_tensors(gvx):
     import torch
     with pytest.raises(ValueError, match="CUDA"):

@@ -519,3 +519,23 @@ def test_dimuon_histogram_parity(gvx, O, dt):
     import synth.device as sd
     dmu, dq, doff = sd.jagged_events(0, off.size - 1, seed=8, dtype=TDT[dt])
     assert torch.equal(dmu, tm) and torch.equal(dq, tq) and torch.equal(doff, to)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_lorentz_transform_parity(gvx, O, dt):
+    v, beta = synth.boost_inputs(np.arange(200_003), dtype=dt, seed=23)
+    b = (0.3, -0.4, 0.5)
+    c, s_ = np.cos(0.7), np.sin(0.7)
+    R = np.array([[c, -s_, 0, 0], [s_, c, 0, 0], [0, 0, 1, 0], [0, 0, 0, 1.0]])
+    Lb = O.boost(np.eye(4), np.array([b] * 4))[0].T
+    L = Lb @ R
+    ref = O.lorentz_transform(v, L)
+    out = host(gvx.lorentz_transform(dev(v), L))
+    S = (np.abs(L) @ np.abs(v.astype(np.float64)).T).T.max(1)  # bound on |L||v| per vector
+    assert boost_violations(out, ref, S, tau_of(dt)).size == 0
+    # in place and SoA give the same bits; a non-Lorentz matrix is a domain error
+    tv = dev(v)
+    gvx.lorentz_transform(tv, L, out=tv)
+    assert np.array_equal(host(tv), out)
+    with pytest.raises(gvx.DomainError):
+        gvx.lorentz_transform(dev(v), 2 * np.eye(4))

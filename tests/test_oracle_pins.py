@@ -516,3 +516,38 @@ def test_dimuon_closed_forms(O):
     # no events
     bins, m, sel = O.dimuon_histogram(np.zeros((0, 4)), np.zeros(0, np.int32), np.zeros(1, np.int64), 0.25, 300.0, 1000)
     assert sel == 0 and m.size == 0
+
+
+# --------------------------------------------------------------------------
+# General 4x4 Lorentz transformation (f2)
+# --------------------------------------------------------------------------
+
+def rot_z(theta):
+    c, s = math.cos(theta), math.sin(theta)
+    return np.array([[c, -s, 0, 0], [s, c, 0, 0], [0, 0, 1, 0], [0, 0, 0, 1.0]])
+
+
+def test_lorentz_transform_pins(O):
+    v, beta = synth.boost_inputs(np.arange(500), seed=19)
+    # a pure boost matrix (columns = oracle boost of the basis) reproduces the uniform boost bitwise (f64)
+    b = (0.3, -0.4, 0.5)
+    L = boost_matrix_from_oracle(O, b)
+    assert np.array_equal(O.lorentz_transform(v, L), O.boost_uniform(v, *b))
+    # a quarter turn about z: (px, py) -> (-py, px) exactly (cos(pi/2) rounds to 6e-17)
+    out = O.lorentz_transform(np.array([[1.0, 2.0, 3.0, 10.0]]), rot_z(math.pi / 2))
+    assert np.allclose(out[0], [-2.0, 1.0, 3.0, 10.0], atol=1e-15)
+    # identity
+    assert np.array_equal(O.lorentz_transform(v, np.eye(4)), v)
+    # composition Λ(β)·R(θ): metric preserved, masses invariant, equals boost(rotate(v))
+    LR = L @ rot_z(0.7)
+    out = O.lorentz_transform(v, LR)
+    two = O.boost_uniform(O.lorentz_transform(v, rot_z(0.7)), *b)
+    assert np.max(np.abs(out - two) / v[:, 3:4]) <= 1e-14
+    m0, _ = O.invariant_mass(v, np.zeros_like(v), coords="pxpypze")
+    m1, _ = O.invariant_mass(out, np.zeros_like(out), coords="pxpypze")
+    assert np.max(np.abs(m1 * np.abs(m1) - m0 * np.abs(m0)) / (v[:, 3] * 3) ** 2) <= 1e-13
+    # not Lorentz (a plain scaling) -> domain error (SPEC.md:191 spirit: invalid transforms rejected)
+    with pytest.raises(O.DomainError):
+        O.lorentz_transform(v, 2 * np.eye(4))
+    with pytest.raises(O.DomainError):
+        O.lorentz_transform(v, np.full((4, 4), np.nan))
