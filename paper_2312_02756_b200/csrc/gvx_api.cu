@@ -268,7 +268,9 @@ gvx_status launch_mass(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, void*
   constexpr int U = (L == L_AOS && sizeof(T) == 8) ? 2 : 1;
   constexpr int G = Group<T, L>::G;
   // f64 AoS: 64-register cap (4 CTAs/SM) measured fastest (sweep ldg1/ldg2).
-  auto k = (sizeof(T) == 8 && L == L_AOS) ? k_invariant_mass<T, C, L, U, 4> : k_invariant_mass<T, C, L, U>;
+  // (if constexpr: instantiate the capped variant only where it is used.)
+  auto k = k_invariant_mass<T, C, L, U>;
+  if constexpr (sizeof(T) == 8 && L == L_AOS) k = k_invariant_mass<T, C, L, U, 4>;
 #ifdef GVX_TUNE
   if constexpr (sizeof(T) == 8 && L == L_AOS && C == C_PTETAPHIM) {
     int v = tune_env("GVX_LDG_CFG");
@@ -341,9 +343,11 @@ gvx_status launch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64
   cudaError_t e;
   if (smem) {
     // f64 AoS: 4 CTAs/SM for the lab histogram, 3 for the heavier CM path (sweep ldg1/ldg4).
-    auto k = (sizeof(T) == 8 && L == L_AOS && !WBO) ? (CM ? k_mass_histogram<T, C, L, CM, true, 3>
-                                                          : k_mass_histogram<T, C, L, CM, true, 4>)
-                                                    : k_mass_histogram<T, C, L, CM, true, 1, WBO>;
+    auto k = k_mass_histogram<T, C, L, CM, true, 1, WBO>;
+    if constexpr (sizeof(T) == 8 && L == L_AOS && !WBO) {
+      if constexpr (CM) k = k_mass_histogram<T, C, L, CM, true, 3>;
+      else k = k_mass_histogram<T, C, L, CM, true, 4>;
+    }
 #ifdef GVX_TUNE
     if constexpr (sizeof(T) == 8 && L == L_AOS && C == C_PTETAPHIM && !WBO) {
       int v = tune_env("GVX_LDG_CFG");
@@ -452,6 +456,25 @@ gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64
   for (int k = 1; k < 4; ++k) aos = aos && (const char*)mu->c[k] == b + k * sizeof(T);
   const size_t nb2 = (size_t)hp.nbins + 2;
   if (nb2 > kMaxSmemBins) return GVX_ERR_UNSUPPORTED;
+  if (aos && aligned(b, 16) && aligned(off, 16) && tma_enabled()) {  // TMA column streaming (AoS muons)
+    using CFG = DimuonTma<T, 1024, 1536, 3, 16>;
+    const size_t smt = CFG::smem_bytes((int)nb2);
+    auto kt = k_dimuon_tma<T, CFG>;
+    int per_sm = smt <= 227 * 1024 ? blocks_per_sm(kt, 32 * (CFG::NCW + 1), smt) : 0;
+    if (per_sm > 0) {
+      const int64_t ntiles = n_events >= CFG::ET + 1 ? (n_events - 1) / CFG::ET : 0;
+      const int64_t full = (int64_t)sm_count() * per_sm;
+      const int grid = (int)(ntiles < 1 ? 1 : (ntiles < full ? ntiles : full));
+      const int64_t chunk = (int64_t)grid << 31;
+      for (int64_t o = 0; o < n_events; o += chunk) {
+        int64_t cn = n_events - o < chunk ? n_events - o : chunk;
+        kt<<<grid, 32 * (CFG::NCW + 1), smt, s>>>((const T*)mu->c[0], q, off + o, cn, hp, bins,
+                                                  m_out ? (T*)m_out + o : nullptr);
+      }
+      cudaError_t e = cudaGetLastError();
+      return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+    }
+  }
   const size_t sm = nb2 * sizeof(unsigned int);
   auto k = aos ? k_dimuon_histogram<T, true> : k_dimuon_histogram<T, false>;
   int grid = grid_for(k, kBlock, sm, kBlock * 4, n_events);

@@ -403,6 +403,136 @@ __global__ void __launch_bounds__(256) k_dimuon_histogram(View4<T> mu, const int
 }
 
 // ============================================================================
+// Jagged dimuon, TMA-fed: the offsets column and the muon column are streamed
+// tile by tile (ET events per tile) into a shared-memory ring. A tile's muon
+// range [offsets[e0], offsets[e0+ET]) is only known from the offsets, so the
+// producer lane reads the two bounds of the NEXT tile with plain loads while
+// the current tile's copies are in flight, then issues one bulk copy of the
+// offsets (ET+2 entries) and one of the muon range. Tiles with more than
+// MAXMU muons (never for the synthetic recipe; possible for real data) set an
+// overflow flag and their consumers read the muons from global memory.
+// Charges are read with plain cached loads (4 B, only for 2-muon events).
+// ============================================================================
+template <typename T, int ET_, int MAXMU_, int STAGES_, int NCW_>
+struct DimuonTma {
+  static constexpr int ET = ET_, MAXMU = MAXMU_, STAGES = STAGES_, NCW = NCW_;
+  static constexpr int NCT = NCW * 32, EPT = ET / NCT;
+  static constexpr int OFF_BYTES = (ET + 2) * 8;
+  static constexpr int MU_BYTES = MAXMU * 4 * (int)sizeof(T);
+  static constexpr int STAGE_BYTES = OFF_BYTES + MU_BYTES;
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int BAR_BYTES = 2 * STAGES * 8 + STAGES * 16;  // full, empty, per-stage {m0, overflow}
+  static_assert(ET % NCT == 0 && ET % 2 == 0 && OFF_BYTES % 16 == 0 && STAGE_BYTES % 16 == 0, "tile geometry");
+  static size_t smem_bytes(int nb2) { return (size_t)RING_BYTES + BAR_BYTES + (size_t)nb2 * 4; }
+};
+
+template <typename T, typename CFG>
+__global__ void __launch_bounds__(32 * (CFG::NCW + 1), 1)
+    k_dimuon_tma(const T* __restrict__ mu, const int32_t* __restrict__ q, const int64_t* __restrict__ offsets,
+                 int64_t n_events, HistParams hp, unsigned long long* __restrict__ bins, T* __restrict__ m_out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CFG::RING_BYTES);
+  uint64_t* empty = full + CFG::STAGES;
+  int64_t* meta = reinterpret_cast<int64_t*>(empty + CFG::STAGES);  // [2*s] = m0, [2*s+1] = overflow
+  unsigned int* sh_hist = reinterpret_cast<unsigned int*>(smem + CFG::RING_BYTES + CFG::BAR_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb2 = hp.nbins + 2;
+  for (int b = threadIdx.x; b < nb2; b += blockDim.x) sh_hist[b] = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CFG::STAGES; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], CFG::NCW);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  // full tiles need offsets[e0 .. e0 + ET + 1] (ET + 2 entries) inside [0, n_events]
+  const int64_t ntiles = n_events >= CFG::ET + 1 ? (n_events - 1) / CFG::ET : 0;
+  auto stage_off = [&](int s) { return reinterpret_cast<int64_t*>(smem + (size_t)s * CFG::STAGE_BYTES); };
+  auto stage_mu = [&](int s) { return reinterpret_cast<T*>(smem + (size_t)s * CFG::STAGE_BYTES + CFG::OFF_BYTES); };
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      const uint64_t pol = tma::policy_evict_first();
+      int64_t t = blockIdx.x;
+      int64_t m0 = 0, m1 = 0;
+      if (t < ntiles) { m0 = __ldg(offsets + t * CFG::ET); m1 = __ldg(offsets + t * CFG::ET + CFG::ET); }
+      for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it % CFG::STAGES, k = it / CFG::STAGES;
+        // bounds of the next tile: in flight while this tile is issued
+        const int64_t tn = t + gridDim.x;
+        int64_t n0 = 0, n1 = 0;
+        if (tn < ntiles) { n0 = __ldg(offsets + tn * CFG::ET); n1 = __ldg(offsets + tn * CFG::ET + CFG::ET); }
+        if (k > 0) {
+          tma::mbar_wait(&empty[s], (k - 1) & 1);
+          tma::fence_proxy_async_smem();
+        }
+        const int64_t cnt = m1 - m0;
+        const bool ov = cnt > CFG::MAXMU || cnt < 0;
+        meta[2 * s] = m0;
+        meta[2 * s + 1] = ov;
+        const uint32_t mub = ov ? 0u : (uint32_t)(cnt * 4 * sizeof(T));
+        tma::mbar_arrive_expect_tx(&full[s], CFG::OFF_BYTES + mub);
+        tma::bulk_g2s(stage_off(s), offsets + t * CFG::ET, CFG::OFF_BYTES, &full[s], pol);
+        if (mub) tma::bulk_g2s(stage_mu(s), mu + 4 * m0, mub, &full[s], pol);
+        m0 = n0;
+        m1 = n1;
+      }
+    }
+  } else {  // consumers
+    const int ctid = threadIdx.x - 32;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int s = it % CFG::STAGES, k = it / CFG::STAGES;
+      tma::mbar_wait(&full[s], k & 1);
+      const int64_t* so = stage_off(s);
+      const T* sm = stage_mu(s);
+      const int64_t m0 = meta[2 * s];
+      const bool ov = meta[2 * s + 1] != 0;
+#pragma unroll
+      for (int u = 0; u < CFG::EPT; ++u) {
+        const int el = u * CFG::NCT + ctid;
+        const int64_t e = t * CFG::ET + el;
+        const int64_t o = so[el], kk = so[el + 1] - o;
+        T M = T(NAN);
+        if (kk == 2 && __ldg(q + o) * __ldg(q + o + 1) < 0) {
+          T a[4], b[4];
+          const T* pa = ov ? mu + 4 * o : sm + 4 * (o - m0);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) { a[c] = pa[c]; b[c] = pa[4 + c]; }
+          M = event_mass<T, C_PTETAPHIM>(a, b);
+          atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+        }
+        if (m_out) m_out[e] = M;
+      }
+      tma::fence_proxy_async_smem();  // all reads of this stage performed before its release
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[s]);
+    }
+    // events not covered by full tiles: the last CTA, plain loads
+    if (blockIdx.x == gridDim.x - 1) {
+      for (int64_t e = ntiles * CFG::ET + ctid; e < n_events; e += CFG::NCT) {
+        const int64_t o = __ldg(offsets + e), kk = __ldg(offsets + e + 1) - o;
+        T M = T(NAN);
+        if (kk == 2 && __ldg(q + o) * __ldg(q + o + 1) < 0) {
+          T a[4], b[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) { a[c] = mu[4 * o + c]; b[c] = mu[4 * o + 4 + c]; }
+          M = event_mass<T, C_PTETAPHIM>(a, b);
+          atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+        }
+        if (m_out) m_out[e] = M;
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
+    unsigned int c = sh_hist[b];
+    if (c) atomicAdd(&bins[b], (unsigned long long)c);
+  }
+}
+
+// ============================================================================
 // K1 / K3 on AoS pairs, TMA-fed (the fast path for the paper's LVector* layout).
 //
 // One CTA = 1 producer warp + NCW consumer warps, persistent over tiles of

@@ -519,6 +519,18 @@ def test_dimuon_histogram_parity(gvx, O, dt):
     import synth.device as sd
     dmu, dq, doff = sd.jagged_events(0, off.size - 1, seed=8, dtype=TDT[dt])
     assert torch.equal(dmu, tm) and torch.equal(dq, tq) and torch.equal(doff, to)
+    # repeat runs are bitwise stable (TMA column ring), and the plain-load kernel (TMA off) agrees
+    for _ in range(5):
+        assert np.array_equal(host(gvx.dimuon_histogram(tm, tq, to)), h)
+    # a tile whose muon range overflows the stage buffer: one event with many muons in the middle
+    big = np.concatenate([mu[: off[5000]], np.tile(mu[:1], (3000, 1)), mu[off[5000]:]])
+    bq = np.concatenate([q[: off[5000]], np.ones(3000, np.int32), q[off[5000]:]])
+    boff = np.concatenate([off[:5001], off[5000:] + 3000])
+    boff[5000] = off[5000]  # event 5000 gets 3000 extra muons (never selected); later offsets shift
+    hb_o, mb_o, sel_b = O.dimuon_histogram(big, bq, boff, LO, HI, NB)
+    mb = torch.empty(boff.size - 1, dtype=TDT[dt], device="cuda")
+    hb = host(gvx.dimuon_histogram(dev(big), dev(bq), dev(boff), m_out=mb))
+    assert int(hb.sum()) == sel_b and np.array_equal(np.isnan(host(mb)), np.isnan(mb_o))
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
