@@ -448,6 +448,26 @@ bool is_lorentz(const double* L) {
 }
 
 // ---------------------------------------------------------- dimuon -------
+template <typename T, typename CFG>
+gvx_status launch_dimuon_tma(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
+                             const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
+  const size_t smt = CFG::smem_bytes(hp.nbins + 2);
+  auto kt = k_dimuon_tma<T, CFG>;
+  int per_sm = smt <= 227 * 1024 ? blocks_per_sm(kt, 32 * (CFG::NCW + 1), smt) : 0;
+  if (per_sm < 1) return GVX_ERR_UNSUPPORTED;
+  const int64_t ntiles = n_events >= CFG::ET + 1 ? (n_events - 1) / CFG::ET : 0;
+  const int64_t full = (int64_t)sm_count() * per_sm;
+  const int grid = (int)(ntiles < 1 ? 1 : (ntiles < full ? ntiles : full));
+  const int64_t chunk = (int64_t)grid << 31;
+  for (int64_t o = 0; o < n_events; o += chunk) {
+    int64_t cn = n_events - o < chunk ? n_events - o : chunk;
+    kt<<<grid, 32 * (CFG::NCW + 1), smt, s>>>((const T*)mu->c[0], q, off + o, cn, hp, bins,
+                                              m_out ? (T*)m_out + o : nullptr);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
 template <typename T>
 gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
                          const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
@@ -456,24 +476,20 @@ gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64
   for (int k = 1; k < 4; ++k) aos = aos && (const char*)mu->c[k] == b + k * sizeof(T);
   const size_t nb2 = (size_t)hp.nbins + 2;
   if (nb2 > kMaxSmemBins) return GVX_ERR_UNSUPPORTED;
-  if (aos && aligned(b, 16) && aligned(off, 16) && tma_enabled()) {  // TMA column streaming (AoS muons)
-    using CFG = DimuonTma<T, 1024, 1536, 3, 16>;
-    const size_t smt = CFG::smem_bytes((int)nb2);
-    auto kt = k_dimuon_tma<T, CFG>;
-    int per_sm = smt <= 227 * 1024 ? blocks_per_sm(kt, 32 * (CFG::NCW + 1), smt) : 0;
-    if (per_sm > 0) {
-      const int64_t ntiles = n_events >= CFG::ET + 1 ? (n_events - 1) / CFG::ET : 0;
-      const int64_t full = (int64_t)sm_count() * per_sm;
-      const int grid = (int)(ntiles < 1 ? 1 : (ntiles < full ? ntiles : full));
-      const int64_t chunk = (int64_t)grid << 31;
-      for (int64_t o = 0; o < n_events; o += chunk) {
-        int64_t cn = n_events - o < chunk ? n_events - o : chunk;
-        kt<<<grid, 32 * (CFG::NCW + 1), smt, s>>>((const T*)mu->c[0], q, off + o, cn, hp, bins,
-                                                  m_out ? (T*)m_out + o : nullptr);
-      }
-      cudaError_t e = cudaGetLastError();
-      return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+  if (aos && aligned(b, 16) && aligned(off, 16) && aligned(q, 16) && tma_enabled()) {  // TMA column streaming
+    gvx_status st = GVX_ERR_UNSUPPORTED;
+#ifdef GVX_TUNE
+    switch (tune_env("GVX_DIMUON_CFG")) {
+      case 1: st = launch_dimuon_tma<T, DimuonTma<T, 512, 768, 6, 16>>(mu, q, off, n_events, hp, bins, m_out, s); break;
+      case 2: st = launch_dimuon_tma<T, DimuonTma<T, 512, 768, 3, 8>>(mu, q, off, n_events, hp, bins, m_out, s); break;
+      case 3: st = launch_dimuon_tma<T, DimuonTma<T, 2048, 2560, 2, 16>>(mu, q, off, n_events, hp, bins, m_out, s); break;
+      case 4: st = launch_dimuon_tma<T, DimuonTma<T, 512, 768, 4, 8>>(mu, q, off, n_events, hp, bins, m_out, s); break;
+      default: break;
     }
+    if (st != GVX_ERR_UNSUPPORTED) return st;
+#endif
+    st = launch_dimuon_tma<T, DimuonTma<T, 1024, 1536, 3, 16>>(mu, q, off, n_events, hp, bins, m_out, s);
+    if (st != GVX_ERR_UNSUPPORTED) return st;
   }
   const size_t sm = nb2 * sizeof(unsigned int);
   auto k = aos ? k_dimuon_histogram<T, true> : k_dimuon_histogram<T, false>;

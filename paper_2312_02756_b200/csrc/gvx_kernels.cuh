@@ -419,21 +419,22 @@ struct DimuonTma {
   static constexpr int NCT = NCW * 32, EPT = ET / NCT;
   static constexpr int OFF_BYTES = (ET + 2) * 8;
   static constexpr int MU_BYTES = MAXMU * 4 * (int)sizeof(T);
-  static constexpr int STAGE_BYTES = OFF_BYTES + MU_BYTES;
+  static constexpr int Q_BYTES = (MAXMU + 8) * 4;  // charges of [m0 & ~3, round_up(m1, 4))
+  static constexpr int STAGE_BYTES = OFF_BYTES + MU_BYTES + Q_BYTES;
   static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
-  static constexpr int BAR_BYTES = 2 * STAGES * 8 + STAGES * 16;  // full, empty, per-stage {m0, overflow}
+  static constexpr int BAR_BYTES = 2 * STAGES * 8 + STAGES * 32;  // full, empty, per-stage {m0, ov, q0, qov}
   static_assert(ET % NCT == 0 && ET % 2 == 0 && OFF_BYTES % 16 == 0 && STAGE_BYTES % 16 == 0, "tile geometry");
   static size_t smem_bytes(int nb2) { return (size_t)RING_BYTES + BAR_BYTES + (size_t)nb2 * 4; }
 };
 
 template <typename T, typename CFG>
-__global__ void __launch_bounds__(32 * (CFG::NCW + 1), 1)
+__global__ void __launch_bounds__(32 * (CFG::NCW + 1))
     k_dimuon_tma(const T* __restrict__ mu, const int32_t* __restrict__ q, const int64_t* __restrict__ offsets,
                  int64_t n_events, HistParams hp, unsigned long long* __restrict__ bins, T* __restrict__ m_out) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CFG::RING_BYTES);
   uint64_t* empty = full + CFG::STAGES;
-  int64_t* meta = reinterpret_cast<int64_t*>(empty + CFG::STAGES);  // [2*s] = m0, [2*s+1] = overflow
+  int64_t* meta = reinterpret_cast<int64_t*>(empty + CFG::STAGES);  // [4s] m0, [4s+1] mu overflow, [4s+2] q0, [4s+3] q overflow
   unsigned int* sh_hist = reinterpret_cast<unsigned int*>(smem + CFG::RING_BYTES + CFG::BAR_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb2 = hp.nbins + 2;
@@ -450,10 +451,14 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), 1)
   const int64_t ntiles = n_events >= CFG::ET + 1 ? (n_events - 1) / CFG::ET : 0;
   auto stage_off = [&](int s) { return reinterpret_cast<int64_t*>(smem + (size_t)s * CFG::STAGE_BYTES); };
   auto stage_mu = [&](int s) { return reinterpret_cast<T*>(smem + (size_t)s * CFG::STAGE_BYTES + CFG::OFF_BYTES); };
+  auto stage_q = [&](int s) {
+    return reinterpret_cast<int32_t*>(smem + (size_t)s * CFG::STAGE_BYTES + CFG::OFF_BYTES + CFG::MU_BYTES);
+  };
 
   if (warp == 0) {
     if (lane == 0) {  // producer
       const uint64_t pol = tma::policy_evict_first();
+      const int64_t n_mu = __ldg(offsets + n_events);  // charges are copied in 16-byte units inside [0, n_mu)
       int64_t t = blockIdx.x;
       int64_t m0 = 0, m1 = 0;
       if (t < ntiles) { m0 = __ldg(offsets + t * CFG::ET); m1 = __ldg(offsets + t * CFG::ET + CFG::ET); }
@@ -469,12 +474,18 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), 1)
         }
         const int64_t cnt = m1 - m0;
         const bool ov = cnt > CFG::MAXMU || cnt < 0;
-        meta[2 * s] = m0;
-        meta[2 * s + 1] = ov;
+        const int64_t q0 = m0 & ~(int64_t)3, q1 = (m1 + 3) & ~(int64_t)3;
+        const bool qov = ov || q1 > n_mu;
+        meta[4 * s] = m0;
+        meta[4 * s + 1] = ov;
+        meta[4 * s + 2] = q0;
+        meta[4 * s + 3] = qov;
         const uint32_t mub = ov ? 0u : (uint32_t)(cnt * 4 * sizeof(T));
-        tma::mbar_arrive_expect_tx(&full[s], CFG::OFF_BYTES + mub);
+        const uint32_t qb = qov ? 0u : (uint32_t)((q1 - q0) * 4);
+        tma::mbar_arrive_expect_tx(&full[s], CFG::OFF_BYTES + mub + qb);
         tma::bulk_g2s(stage_off(s), offsets + t * CFG::ET, CFG::OFF_BYTES, &full[s], pol);
         if (mub) tma::bulk_g2s(stage_mu(s), mu + 4 * m0, mub, &full[s], pol);
+        if (qb) tma::bulk_g2s(stage_q(s), q + q0, qb, &full[s], pol);
         m0 = n0;
         m1 = n1;
       }
@@ -487,27 +498,37 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), 1)
       tma::mbar_wait(&full[s], k & 1);
       const int64_t* so = stage_off(s);
       const T* sm = stage_mu(s);
-      const int64_t m0 = meta[2 * s];
-      const bool ov = meta[2 * s + 1] != 0;
+      const int64_t m0 = meta[4 * s], q0 = meta[4 * s + 2];
+      const bool ov = meta[4 * s + 1] != 0, qov = meta[4 * s + 3] != 0;
+      const int32_t* sq = stage_q(s);
+      // phase 1: this thread's events out of the stage into registers, then release it
+      bool sel[CFG::EPT];
+      T a[CFG::EPT][4], b[CFG::EPT][4];
 #pragma unroll
       for (int u = 0; u < CFG::EPT; ++u) {
         const int el = u * CFG::NCT + ctid;
-        const int64_t e = t * CFG::ET + el;
         const int64_t o = so[el], kk = so[el + 1] - o;
-        T M = T(NAN);
-        if (kk == 2 && __ldg(q + o) * __ldg(q + o + 1) < 0) {
-          T a[4], b[4];
+        const int32_t* pq = qov ? q + o : sq + (o - q0);
+        sel[u] = kk == 2 && pq[0] * pq[1] < 0;
+        if (sel[u]) {
           const T* pa = ov ? mu + 4 * o : sm + 4 * (o - m0);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) { a[c] = pa[c]; b[c] = pa[4 + c]; }
-          M = event_mass<T, C_PTETAPHIM>(a, b);
-          atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+          for (int c = 0; c < 4; ++c) { a[u][c] = pa[c]; b[u][c] = pa[4 + c]; }
         }
-        if (m_out) m_out[e] = M;
       }
       tma::fence_proxy_async_smem();  // all reads of this stage performed before its release
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
+      // phase 2: masses and bins while the ring refills
+#pragma unroll
+      for (int u = 0; u < CFG::EPT; ++u) {
+        T M = T(NAN);
+        if (sel[u]) {
+          M = event_mass<T, C_PTETAPHIM>(a[u], b[u]);
+          atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+        }
+        if (m_out) m_out[t * CFG::ET + u * CFG::NCT + ctid] = M;
+      }
     }
     // events not covered by full tiles: the last CTA, plain loads
     if (blockIdx.x == gridDim.x - 1) {
