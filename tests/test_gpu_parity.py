@@ -551,3 +551,41 @@ def test_lorentz_transform_parity(gvx, O, dt):
     assert np.array_equal(host(tv), out)
     with pytest.raises(gvx.DomainError):
         gvx.lorentz_transform(dev(v), 2 * np.eye(4))
+
+
+def test_cuda_graph_capture(gvx):
+    """The ABI only enqueues on the caller's stream (no allocation, no sync), so a whole step
+    can be captured into a CUDA graph and replayed — the launch-bound small-N regime's answer."""
+    import synth.device as sd
+    n = 50_000
+    v1, v2 = sd.muon_pairs(n, dtype=torch.float64)
+    bv, bb = sd.boost_inputs(n, dtype=torch.float64)
+    m = torch.empty(n, dtype=torch.float64, device="cuda")
+    bo = torch.empty((n, 4), dtype=torch.float64, device="cuda")
+    bins = gvx.new_bins()
+    binc = gvx.new_bins()
+
+    def step():
+        bins.zero_()
+        binc.zero_()
+        gvx.invariant_mass(v1, v2, out=m)
+        gvx.boost(bv, bb, out=bo)
+        gvx.mass_histogram(v1, v2, bins=bins)
+        gvx.mass_histogram(v1, v2, bins=binc, cm=True)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()  # warm-up outside capture (occupancy queries, smem opt-in)
+    torch.cuda.current_stream().wait_stream(s)
+    ref = [t.clone() for t in (m, bo, bins, binc)]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    m.zero_()
+    bo.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip((m, bo, bins, binc), ref):
+        assert torch.equal(a, b)
