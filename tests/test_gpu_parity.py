@@ -589,3 +589,31 @@ def test_cuda_graph_capture(gvx):
     torch.cuda.synchronize()
     for a, b in zip((m, bo, bins, binc), ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dt", [torch.float64, torch.float32])
+def test_physics_invariants_full_size(gvx, dt):
+    """Properties that hold at any size, checked on all 1e8 pairs of the bench batch:
+    pair symmetry (bitwise: every step of the formula is symmetric), and invariance of M
+    under a common rotation about z (φ → φ + δ) and under the reflection η → −η of both
+    vectors (within the north-star tolerance, scale E_lab² ≤ (2 Σ pt cosh η)²)."""
+    import synth.device as sd
+    n = 100_000_000
+    v1, v2 = sd.muon_pairs(n, dtype=dt)
+    m = gvx.invariant_mass(v1, v2)
+    assert torch.equal(gvx.invariant_mass(v2, v1), m)
+    tau = 1e-12 if dt == torch.float64 else 1e-5
+    e = (v1[:, 0] * torch.cosh(v1[:, 1]) + v2[:, 0] * torch.cosh(v2[:, 1])).double() + 1.0
+    for k, delta in ((2, 0.37), (1, None)):
+        w1, w2 = v1.clone(), v2.clone()
+        if delta is None:
+            w1[:, 1].neg_()
+            w2[:, 1].neg_()
+        else:
+            w1[:, 2] += delta
+            w2[:, 2] += delta
+        mr = gvx.invariant_mass(w1, w2)
+        md, mrd = m.double(), mr.double()
+        err = (md * md.abs() - mrd * mrd.abs()).abs() / (e * e)
+        assert err.max().item() <= tau, (k, err.max().item())
+        del w1, w2, mr
