@@ -11,8 +11,13 @@
  * ---------------------------------------------------------------------------
  * Ownership. Every data pointer is caller-owned. Device entry points take
  *   DEVICE pointers valid on the calling thread's current CUDA device; the
- *   library allocates no device memory and keeps no mutable global state
- *   (beyond a per-device SM-count cache filled once). Outputs are
+ *   library allocates no device memory. Its only state is a per-(kernel,
+ *   device) launch-configuration cache (SM count, occupancy, shared-memory
+ *   opt-in), filled on first use under a mutex — so every entry point may be
+ *   called from several host threads and captured into a CUDA graph after one
+ *   warm-up call. Environment: GVX_DISABLE_TMA=1 / GVX_FORCE_TMA=1 pick the
+ *   register (LDG) or shared-memory-ring (TMA) kernels for A/B runs; results
+ *   are identical either way. Outputs are
  *   caller-allocated, as in the paper's kernel signature
  *   `(LVector *v1, LVector *v2, Scalar *m, size_t N)`.
  * Asynchrony. Device entry points enqueue on `stream` and return without a

@@ -68,9 +68,11 @@ int blocks_per_sm(K kernel, int block, size_t smem) {
     }
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess) {
     per_sm = 0;
-  cudaGetLastError();
+    cudaGetLastError();  // clear only the error this query raised
+  }
+  if (per_sm < 1) per_sm = 0;
   std::lock_guard<std::mutex> lk(g_occ_mu);
   g_occ[key] = per_sm;
   return per_sm;
