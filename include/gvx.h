@@ -174,6 +174,36 @@ gvx_status gvx_dimuon_histogram(gvx_dtype dtype, const gvx_vec4_cview *muons, co
                                 int32_t nbins, unsigned long long *bins, void *m_out,
                                 gvx_stream_t stream);
 
+/*
+ * Transfer-inclusive runtime (the host function "handling the
+ * device memory allocation and transfers if necessary").
+ * A pipeline owns device staging (3 slots x 3 buffers of chunk_events
+ * 4-vectors), three CUDA streams and events on the device current at create.
+ * A call cuts a HOST-resident batch into chunks; chunk c's H2D copy, chunk
+ * c-1's kernels and chunk c-2's D2H copy overlap. Calls are asynchronous with
+ * respect to the host: `stream` (the caller's) is made to wait for the whole
+ * call, so host buffers must stay valid and outputs are ready after the
+ * caller synchronises `stream`. Host buffers should be pinned
+ * (cudaHostAlloc / cudaHostRegister) for full PCIe bandwidth. Results are
+ * bitwise those of the device entry points on the same data.
+ *   create:  dtype, chunk_events in [1, 2^31] -> *out (GVX_ERR_CUDA if device
+ *            allocation fails). destroy: waits for the pipeline's work.
+ *   gvx_host_pairs: n AoS pairs (h_v1, h_v2, layout by `coords`); any of
+ *            h_m_out (n masses), h_bins / h_bins_cm (nbins+2 uint64 each,
+ *            OVERWRITTEN with this batch's lab / CM histogram) may be NULL.
+ *   gvx_host_boost: n PxPyPzE vectors h_v, n betas h_beta (AoS [n][3]),
+ *            h_out (n vectors).
+ */
+typedef struct gvx_host_pipeline gvx_host_pipeline;
+gvx_status gvx_host_pipeline_create(gvx_dtype dtype, int64_t chunk_events, gvx_host_pipeline **out);
+gvx_status gvx_host_pipeline_destroy(gvx_host_pipeline *p);
+gvx_status gvx_host_pairs(gvx_host_pipeline *p, gvx_coords coords, const void *h_v1, const void *h_v2,
+                          int64_t n, double lo, double hi, int32_t nbins, void *h_m_out,
+                          unsigned long long *h_bins, unsigned long long *h_bins_cm,
+                          gvx_stream_t stream);
+gvx_status gvx_host_boost(gvx_host_pipeline *p, const void *h_v, const void *h_beta, int64_t n,
+                          void *h_out, gvx_stream_t stream);
+
 /* Human-readable name of a status code (static storage). */
 const char *gvx_status_string(gvx_status status);
 /* The CUDA error string behind the last GVX_ERR_CUDA on this thread. */

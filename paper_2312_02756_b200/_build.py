@@ -18,12 +18,13 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-
 
 TARGETS = {
     os.path.join(PKG, "libgvx.so"): {
-        "main": os.path.join(PKG, "csrc", "gvx_api.cu"),
-        "deps": [os.path.join(PKG, "csrc", f) for f in ("gvx_api.cu", "gvx_kernels.cuh", "gvx_math.cuh", "gvx_tma.cuh")]
+        "main": [os.path.join(PKG, "csrc", "gvx_api.cu"), os.path.join(PKG, "csrc", "gvx_host.cu")],
+        "deps": [os.path.join(PKG, "csrc", f)
+                 for f in ("gvx_api.cu", "gvx_host.cu", "gvx_kernels.cuh", "gvx_math.cuh", "gvx_tma.cuh")]
         + [os.path.join(ROOT, "include", "gvx.h")],
     },
     os.path.join(ROOT, "tools", "libgvx_tune.so"): {
-        "main": os.path.join(PKG, "csrc", "gvx_api.cu"),
+        "main": [os.path.join(PKG, "csrc", "gvx_api.cu"), os.path.join(PKG, "csrc", "gvx_host.cu")],
         "deps": [os.path.join(PKG, "csrc", f) for f in ("gvx_api.cu", "gvx_kernels.cuh", "gvx_math.cuh", "gvx_tma.cuh")]
         + [os.path.join(ROOT, "include", "gvx.h")],
         "extra": ["-DGVX_TUNE"],
@@ -51,7 +52,8 @@ def build(force: bool = False, verbose: bool = False, tune: bool = False) -> Non
             continue
         if not force and not _stale(out, spec["deps"]):
             continue
-        cmd = [NVCC] + COMMON + spec.get("extra", []) + ["-o", out + ".tmp", spec["main"]]
+        mains = spec["main"] if isinstance(spec["main"], list) else [spec["main"]]
+        cmd = [NVCC] + COMMON + spec.get("extra", []) + ["-o", out + ".tmp"] + mains
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
