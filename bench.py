@@ -475,7 +475,7 @@ def run_e2e(args, gvx, v1, v2, bv, bb, dev, stream, world):
     return {"value": passes * host_n * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
             "h2d_bytes_per_step": passes * pipe.h2d_bytes, "d2h_bytes_per_step": passes * pipe.d2h_bytes,
             "steps": steps, "host_batch_events": host_n, "passes_per_step": passes,
-            "path": "pinned host -> chunked H2D/compute/D2H over 3 streams (hostpipe)"}
+            "path": "pinned host -> native gvx_host_pipeline (C ABI): chunked H2D / kernels / D2H overlapped on 3 streams"}
 
 
 
