@@ -102,6 +102,23 @@ def test_lorentz_matrix_validation(gvx):
     assert L.gvx_lorentz_transform(gvx.GVX_F64, by(a), None, by(o), 4, None) == 1
 
 
+def test_host_pipeline_validation():
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2312_02756_b200", "libgvx.so"))
+    P = ctypes.c_void_p
+    lib.gvx_host_pipeline_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.POINTER(P)]
+    lib.gvx_host_pairs.argtypes = [P, ctypes.c_int, P, P, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_int32, P, P, P, P]
+    lib.gvx_host_boost.argtypes = [P, P, P, ctypes.c_int64, P, P]
+    lib.gvx_host_pipeline_destroy.argtypes = [P]
+    out = P()
+    assert lib.gvx_host_pipeline_create(9, 1024, ctypes.byref(out)) == 1          # bad dtype
+    assert lib.gvx_host_pipeline_create(1, 0, ctypes.byref(out)) == 1             # chunk < 1
+    assert lib.gvx_host_pipeline_create(1, 1 << 40, ctypes.byref(out)) == 1       # chunk > 2^31
+    assert lib.gvx_host_pairs(None, 0, None, None, 4, 0.0, 1.0, 10, None, None, None, None) == 1
+    assert lib.gvx_host_boost(None, None, None, 4, None, None) == 1
+    assert lib.gvx_host_pipeline_destroy(None) == 1
+
+
 def test_python_binding_rejects_cpu_tensors(gvx):
     import torch
     with pytest.raises(ValueError, match="CUDA"):
