@@ -617,3 +617,83 @@ def test_physics_invariants_full_size(gvx, dt):
         err = (md * md.abs() - mrd * mrd.abs()).abs() / (e * e)
         assert err.max().item() <= tau, (k, err.max().item())
         del w1, w2, mr
+
+
+def _layout_views(t, kind, rng):
+    """Return a view of the [n, 4] CUDA tensor t with the requested memory layout (same values)."""
+    n = t.shape[0]
+    if kind == "aos":
+        return t
+    if kind == "aos_offset":  # misaligned base (one scalar offset)
+        buf = torch.empty(n * 4 + 1, dtype=t.dtype, device=t.device)
+        v = buf[1:].view(n, 4)
+        v.copy_(t)
+        return v
+    if kind == "soa":
+        return [t[:, k].contiguous() for k in range(4)]
+    if kind == "soa_offset":
+        out = []
+        for k in range(4):
+            buf = torch.empty(n + 3, dtype=t.dtype, device=t.device)
+            buf[3:].copy_(t[:, k])
+            out.append(buf[3:])
+        return out
+    if kind.startswith("strided"):
+        s = int(kind[len("strided"):])
+        buf = torch.zeros((n, s), dtype=t.dtype, device=t.device)
+        buf[:, :4].copy_(t)
+        return buf[:, :4]
+    raise ValueError(kind)
+
+
+def test_dispatch_fuzz(gvx, O):
+    """Random sizes x layouts x coordinate systems x dtypes x operations against the oracle —
+    exercises every dispatch branch (TMA ring AoS/SoA, LDG AoS/SoA/strided, tails, misaligned
+    views) with the same parity predicates as the targeted tests."""
+    rng = np.random.default_rng(2024)
+    kinds = ["aos", "aos_offset", "soa", "soa_offset", "strided5", "strided8"]
+    for trial in range(36):
+        dt = [np.float32, np.float64][trial % 2]
+        coords = ["ptetaphim", "pxpypze", "pxpypzm", "ptetaphie"][rng.integers(4)]
+        n = int(rng.choice([0, 1, 3, 31, 257, 4097, int(rng.integers(1, 300_000))]))
+        kind1, kind2 = rng.choice(kinds, 2)
+        op = ["mass", "hist", "cm"][trial % 3]
+        v1, v2 = synth.muon_pairs(np.arange(n), seed=100 + trial, dtype=dt)
+        if coords == "pxpypze":
+            v1, _ = synth.boost_inputs(np.arange(n), seed=200 + trial, dtype=dt)
+            v2, _ = synth.boost_inputs(np.arange(n), seed=300 + trial, dtype=dt)
+        elif coords == "pxpypzm":
+            a, _ = synth.boost_inputs(np.arange(n), seed=200 + trial, dtype=dt)
+            b, _ = synth.boost_inputs(np.arange(n), seed=300 + trial, dtype=dt)
+            v1 = np.concatenate([a[:, :3], np.full((n, 1), synth.MUON_MASS, dt)], 1).astype(dt)
+            v2 = np.concatenate([b[:, :3], np.full((n, 1), synth.MUON_MASS, dt)], 1).astype(dt)
+        elif coords == "ptetaphie":
+            v1 = v1.copy()
+            v2 = v2.copy()
+            v1[:, 3] = (v1[:, 0] * np.cosh(v1[:, 1].astype(np.float64)) * 1.01).astype(dt)
+            v2[:, 3] = (v2[:, 0] * np.cosh(v2[:, 1].astype(np.float64)) * 1.01).astype(dt)
+        t1 = _layout_views(torch.from_numpy(v1).cuda().reshape(n, 4), kind1, rng)
+        t2 = _layout_views(torch.from_numpy(v2).cuda().reshape(n, 4), kind2, rng)
+        tag = (trial, dt.__name__, coords, n, kind1, kind2, op)
+        z = np.zeros_like(v1)
+        _, e1 = O.invariant_mass(v1, z, coords=coords)
+        _, e2 = O.invariant_mass(v2, z, coords=coords)
+        e = np.abs(e1.astype(np.float64)) + np.abs(e2.astype(np.float64)) + 1e-30
+        if coords in ("pxpypze", "pxpypzm"):
+            e = e + np.sqrt((v1[:, :3].astype(np.float64) ** 2).sum(1)) + np.sqrt((v2[:, :3].astype(np.float64) ** 2).sum(1))
+        if op == "mass":
+            mo, _ = O.invariant_mass(v1, v2, coords=coords)
+            m = host(gvx.invariant_mass(t1, t2, coords=coords))
+            assert mass_violations(m, mo, e, tau_of(dt)).size == 0, tag
+        else:
+            cm = op == "cm"
+            h = host(gvx.mass_histogram(t1, t2, coords=coords, cm=cm))
+            ho, mo = O.mass_histogram(v1, v2, LO, HI, NB, cm=cm, coords=coords)
+            assert int(h.sum()) == n, tag
+            if cm:
+                mlab, _ = O.invariant_mass(v1, v2, coords=coords)
+                nanp = np.isnan(mo) | (np.abs(mlab.astype(np.float64)) < (1e-2 if dt == np.float32 else 1e-6) * e)
+                fails, _ = hist_check(h, mo, e, tau_of(dt), LO, HI, NB, nan_possible=nanp, m_window_center=mlab)
+            else:
+                fails, _ = hist_check(h, mo, e, tau_of(dt), LO, HI, NB)
+            assert not fails, (tag, fails)
