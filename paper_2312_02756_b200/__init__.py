@@ -160,6 +160,9 @@ def _view(x: VecArg, ncomp: int, name: str, writable: bool = False):
         s0, s1 = x.stride()
         n = x.shape[0]
         ptrs = [base + k * s1 * es for k in range(ncomp)]
+        if n > 1 and s0 < 1:
+            raise ValueError(f"{name}: row stride {s0} is not supported (broadcast or flipped views); "
+                             "make the tensor contiguous")
         stride = s0 if n > 1 else max(s0, 1)
         dtype, dev = x.dtype, x.device
         keep = (x,)
@@ -179,6 +182,8 @@ def _view(x: VecArg, ncomp: int, name: str, writable: bool = False):
         if len(strides) != 1:
             raise ValueError(f"{name}: components must share one stride")
         stride = strides.pop()
+        if stride < 1:
+            raise ValueError(f"{name}: stride {stride} is not supported (broadcast or flipped views)")
         ptrs = [c.data_ptr() for c in comps]
         keep = tuple(comps)
     if ncomp == 4:

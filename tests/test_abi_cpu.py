@@ -133,3 +133,13 @@ def test_oracle_is_test_infrastructure_only():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).lower().replace("no oracle", ""), f
+
+
+def test_binding_rejects_unsupported_strides(gvx, monkeypatch):
+    """Broadcast (stride 0) views are rejected before any call (checked with a fake CUDA tensor
+    flag: _view only inspects shapes and strides)."""
+    import torch
+    t = torch.zeros(1, 4, dtype=torch.float64).expand(5, 4)
+    monkeypatch.setattr(gvx, "_require_cuda", lambda x, name: None)
+    with pytest.raises(ValueError, match="stride"):
+        gvx._view(t, 4, "v1")
