@@ -548,7 +548,7 @@ gvx_status gvx_dimuon_histogram(gvx_dtype dtype, const gvx_vec4_cview* muons, co
       !aligned(bins, 8))
     return GVX_ERR_INVALID_ARGUMENT;
   if (m_out && !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
-  HistParams hp{lo, hi, hi - lo, 1.0 / (hi - lo), (double)nbins, nbins};
+  const HistParams hp = make_hist_params(lo, hi, nbins);
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == GVX_F64) return launch_dimuon<double>(muons, charge, offsets, n_events, hp, bins, m_out, s);
   return launch_dimuon<float>(muons, charge, offsets, n_events, hp, bins, m_out, s);
@@ -617,7 +617,7 @@ gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4
   if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !bins || !aligned(bins, 8)) return GVX_ERR_INVALID_ARGUMENT;
   if (m_out && !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
   if (boosted_out && !out_view_ok(boosted_out, es)) return GVX_ERR_INVALID_ARGUMENT;
-  HistParams hp{lo, hi, hi - lo, 1.0 / (hi - lo), (double)nbins, nbins};
+  const HistParams hp = make_hist_params(lo, hi, nbins);
   cudaStream_t s = (cudaStream_t)stream;
 #define GVX_HIST_DISPATCH(T, C)                                                                                  \
   (cm ? dispatch_hist<T, C, true>(v1, v2, n, hp, bins, m_out, boosted_out, s)                       \

@@ -638,11 +638,11 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
   if (warp == 0) {
     if (lane == 0) {  // producer
       const uint64_t pol = tma::policy_evict_first();
-      int it = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int s = it % CFG::STAGES, k = it / CFG::STAGES;
-        if (k > 0) {
-          tma::mbar_wait(&empty[s], (k - 1) & 1);
+      int s = 0, it = 0;
+      uint32_t ph = 1;  // parity of the empty-barrier phase to wait for (round k-1)
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (it >= CFG::STAGES) {
+          tma::mbar_wait(&empty[s], ph);
           tma::fence_proxy_async_smem();  // consumers' reads before the async-proxy refill
         }
         tma::mbar_arrive_expect_tx(&full[s], CFG::STAGE_BYTES);
@@ -657,14 +657,16 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
           tma::bulk_g2s(dst, v1.c[0] + t * TV, CFG::HALF, &full[s], pol);
           tma::bulk_g2s(dst + TV, v2.c[0] + t * TV, CFG::HALF, &full[s], pol);
         }
+        ++it;
+        if (++s == CFG::STAGES) { s = 0; ph ^= 1u; }
       }
     }
   } else {  // consumers
     const int ctid = threadIdx.x - 32;
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int s = it % CFG::STAGES, k = it / CFG::STAGES;
-      tma::mbar_wait(&full[s], k & 1);
+    int s = 0;
+    uint32_t ph = 0;  // parity of the full-barrier phase of this round
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      tma::mbar_wait(&full[s], ph);
       const T* src = ring + (size_t)s * 2 * TV;
       T a[CFG::EPT][4], b[CFG::EPT][4];
 #pragma unroll
@@ -699,6 +701,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
       for (int u = 0; u < CFG::EPT; ++u)
         pair_consume<T, COORDS, MODE, WANT_BO>(a[u], b[u], t * CFG::TILE + u * CFG::NCT + ctid, m_out, sh_hist, hp,
                                                bo);
+      if (++s == CFG::STAGES) { s = 0; ph ^= 1u; }
     }
     // ragged tail (< TILE events): the last CTA, plain loads
     if (blockIdx.x == gridDim.x - 1) {

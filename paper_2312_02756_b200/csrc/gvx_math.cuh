@@ -28,6 +28,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 namespace gvx {
 
@@ -99,10 +100,28 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   double e = fma(-x * y, y, 1.0);
   return fma(y * e, fma(e, 0.375, 0.5), y);
 }
-// sqrt(x) for x >= 0 (x = 0 -> 0), <= 3 ulp: x * rsqrt(x).
+// sqrt(x), <= 3 ulp: x * rsqrt(x). x below the smallest normal (zero,
+// denormal) or negative -> +0 (the E^2 clamp of reading R2 comes for free);
+// the test is an integer compare of the high word (ALU pipe), not a DSETP on
+// the FP64 pipe, which bounds the fp64 kernels. For finite x only (a NaN
+// with the sign bit set would give 0): the fast domain produces no NaN here.
 __device__ __forceinline__ double fast_sqrt(double x) {
   double s = x * fast_rsqrt(x);
-  return x > 0.0 ? s : 0.0 * x;  // keeps +0, NaN propagates via 0*NaN
+  return __double2hiint(x) < 0x00100000 ? 0.0 : s;
+}
+// sqrt(|x|) for any x: NaN -> NaN whatever its sign bit (the FP64 units
+// return a NaN with the sign bit set, so the test is on |x|'s bits, not on
+// the result of a DADD-implemented fabs), |x| below the smallest normal -> 0.
+__device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double2hiint(x) & 0x7fffffffu; }
+__device__ __forceinline__ double fast_sqrt_abs(double x) {
+  double ax = fabs(x);
+  double s = ax * fast_rsqrt(ax);
+  return abs_hi(x) < 0x00100000u ? 0.0 : s;
+}
+// sign(m2) * sqrt(|m2|) with the sign bit copied by an integer OR (m2 = -0
+// gives -0, as the oracle's sqrt(-0) does).
+__device__ __forceinline__ double copy_sign_bit(double r, double m2) {
+  return __hiloint2double(__double2hiint(r) | (__double2hiint(m2) & (int)0x80000000), __double2loint(r));
 }
 
 // Exact power of two 2^k for |k| < 1000 (integer ops only).
@@ -245,17 +264,19 @@ __device__ __noinline__ T pair_mass_exact(T pt1, T eta1, T phi1, T m1, T pt2, T 
 // Fast domain and fast pair mass.
 // ---------------------------------------------------------------------------
 // Fast domain, tested on the high words with integer compares (ALU pipe):
-// |eta| < 20, |phi| < 1024, |pt|, |m| < 2^200; NaN/Inf fail every test.
-__device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double2hiint(x) & 0x7fffffffu; }
+// |eta| < 20, |phi| < 1024, 2^-200 <= |pt| < 2^200, |m| < 2^200; NaN/Inf fail
+// every test. The lower bound on pt keeps every square normal (pt = 0 and
+// denormal-scale vectors take the literal cold path).
 __device__ __forceinline__ bool fast_domain(double pt, double eta, double phi, double m) {
-  return (abs_hi(eta) < 0x40340000u) & (abs_hi(phi) < 0x40900000u) & (abs_hi(pt) < 0x4C700000u) &
-         (abs_hi(m) < 0x4C700000u);
+  return (abs_hi(eta) < 0x40340000u) & (abs_hi(phi) < 0x40900000u) &
+         (abs_hi(pt) - 0x33700000u < 0x4C700000u - 0x33700000u) & (abs_hi(m) < 0x4C700000u);
 }
-// f32: |eta| < 20, |phi| < 8, |pt|, |m| < 2^20.
+// f32: |eta| < 20, |phi| < 8, 2^-40 <= |pt| < 2^20, |m| < 2^20 (the MUFU
+// sqrt flushes denormals, so pt^2 must stay normal).
 __device__ __forceinline__ uint32_t abs_bits(float x) { return (uint32_t)__float_as_int(x) & 0x7fffffffu; }
 __device__ __forceinline__ bool fast_domain(float pt, float eta, float phi, float m) {
-  return (abs_bits(eta) < 0x41A00000u) & (abs_bits(phi) < 0x41000000u) & (abs_bits(pt) < 0x49800000u) &
-         (abs_bits(m) < 0x49800000u);
+  return (abs_bits(eta) < 0x41A00000u) & (abs_bits(phi) < 0x41000000u) &
+         (abs_bits(pt) - 0x2B800000u < 0x49800000u - 0x2B800000u) & (abs_bits(m) < 0x49800000u);
 }
 
 __device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double phi1, double m1, double pt2,
@@ -273,8 +294,7 @@ __device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double
   double t = (c1 ? -P1 : mm1) + (c2 ? -P2 : mm2);
   double A12 = (c1 | c2) ? 0.0 : A1 * A2;
   double m2sq = t + 2.0 * (fast_sqrt(A12) - pt1 * pt2 * (c + sh1 * sh2));
-  double r = fast_sqrt(fabs(m2sq));
-  return m2sq >= 0.0 ? r : -r;
+  return copy_sign_bit(fast_sqrt_abs(m2sq), m2sq);
 }
 
 // fp32: MUFU-based cos/exp/rcp/sqrt (error budget DESIGN.md §5: <= ~1e-6 E^2
@@ -340,7 +360,7 @@ __device__ __forceinline__ V4<double> ptetaphim_fast(double pt, double eta, doub
   o.x = pt * c;
   o.y = pt * s;
   o.z = pt * sh;
-  o.t = fast_sqrt(fmax(fma(m, fabs(m), q * q), 0.0));
+  o.t = fast_sqrt(fma(m, fabs(m), q * q));  // negative E^2 -> 0 (R2)
   return o;
 }
 __device__ __forceinline__ V4<float> ptetaphim_fast(float pt, float eta, float phi, float m) {
@@ -386,14 +406,17 @@ __device__ __forceinline__ BoostCoef<T> boost_coef(T bx, T by, T bz) {
 }
 // Fast coefficients (MUFU seeds + Newton, <= 2 ulp) for the CM histogram,
 // whose fp64 variant is FP64-pipe bound.
+// With u = 1 - beta^2: gamma = u^-1/2 and gamma^2/(1+gamma) = 1/(u + u gamma)
+// (one reciprocal, no DMULs); beta^2 < 1 <=> u > 0, tested on u's high word
+// (u >= 2^-53 whenever beta^2 < 1; NaN passes and propagates).
 __device__ __forceinline__ BoostCoef<double> boost_coef_fast(double bx, double by, double bz) {
   BoostCoef<double> k;
   k.bx = bx; k.by = by; k.bz = bz;
-  double b2 = bx * bx + by * by + bz * bz;
-  k.ok = b2 < 1.0;
-  double g = fast_rsqrt(1.0 - b2);
+  double u = 1.0 - (bx * bx + by * by + bz * bz);
+  k.ok = __double2hiint(u) > 0;
+  double g = fast_rsqrt(u);
   k.g = g;
-  k.bg = g * g * fast_rcp(1.0 + g);
+  k.bg = fast_rcp(fma(u, g, u));
   return k;
 }
 __device__ __forceinline__ BoostCoef<float> boost_coef_fast(float bx, float by, float bz) {
@@ -408,7 +431,10 @@ __device__ __forceinline__ BoostCoef<float> boost_coef_fast(float bx, float by, 
   return k;
 }
 
-template <typename T>
+// Y0: v.y is exactly zero (the CM path's vector 1 in its rotated frame), so
+// the y terms of the products are skipped (exact: adding a +-0 product to a
+// sum changes at most the sign of a zero).
+template <typename T, bool Y0 = false>
 __device__ __forceinline__ V4<T> apply_boost(const BoostCoef<T>& k, const V4<T>& v) {
   V4<T> o;
   if (!k.ok) {
@@ -416,10 +442,10 @@ __device__ __forceinline__ V4<T> apply_boost(const BoostCoef<T>& k, const V4<T>&
     o.x = o.y = o.z = o.t = nan;
     return o;
   }
-  T bp = k.bx * v.x + k.by * v.y + k.bz * v.z;
+  T bp = Y0 ? k.bx * v.x + k.bz * v.z : k.bx * v.x + k.by * v.y + k.bz * v.z;
   T f = k.bg * bp + k.g * v.t;
   o.x = v.x + f * k.bx;
-  o.y = v.y + f * k.by;
+  o.y = Y0 ? f * k.by : v.y + f * k.by;
   o.z = v.z + f * k.bz;
   o.t = k.g * (v.t + bp);
   return o;
@@ -429,10 +455,7 @@ __device__ __forceinline__ double any_rcp(double x) { return fast_rcp(x); }
 __device__ __forceinline__ float any_rcp(float x) { return fast_rcp(x); }
 
 // Signed square root with the fast sqrt (fp64: MUFU.RSQ64H + Newton, <= 3 ulp).
-__device__ __forceinline__ double fast_signed_sqrt(double m2) {
-  double r = fast_sqrt(fabs(m2));
-  return m2 >= 0.0 ? r : -r;
-}
+__device__ __forceinline__ double fast_signed_sqrt(double m2) { return copy_sign_bit(fast_sqrt_abs(m2), m2); }
 __device__ __forceinline__ float fast_signed_sqrt(float m2) {
   float r = fast_sqrt(fabsf(m2));
   return m2 >= 0.f ? r : -r;
@@ -441,16 +464,19 @@ __device__ __forceinline__ float fast_signed_sqrt(float m2) {
 // CM-frame mass (reading R11): beta_cm = -P/E, boost both, sum, signed mass.
 // E <= 0 or beta^2 >= 1 (or NaN) -> gamma = NaN, so every output is NaN
 // without a branch.
-template <typename T>
+__device__ __forceinline__ bool is_positive(double x) { return __double2hiint(x) > 0; }  // x >= 2^-1022 (or +NaN)
+__device__ __forceinline__ bool is_positive(float x) { return x > 0.f; }
+
+template <typename T, bool A_Y0 = false>
 __device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>* a_out, V4<T>* b_out) {
   T Px = a.x + b.x, Py = a.y + b.y, Pz = a.z + b.z, E = a.t + b.t;
   T inv = any_rcp(E);
   BoostCoef<T> k = boost_coef_fast(-Px * inv, -Py * inv, -Pz * inv);
-  const bool ok = k.ok && (E > T(0));
+  const bool ok = k.ok && is_positive(E);
   k.g = ok ? k.g : T(NAN);
   k.bg = ok ? k.bg : T(NAN);
   k.ok = true;
-  V4<T> a2 = apply_boost(k, a), b2 = apply_boost(k, b);
+  V4<T> a2 = apply_boost<T, A_Y0>(k, a), b2 = apply_boost(k, b);
   if (a_out) { *a_out = a2; *b_out = b2; }
   T X = a2.x + b2.x, Y = a2.y + b2.y, Z = a2.z + b2.z, W = a2.t + b2.t;
   return fast_signed_sqrt(W * W - (X * X + Y * Y + Z * Z));
@@ -464,7 +490,7 @@ __device__ __forceinline__ void sinh_cosh(float x, float& sh, float& ch) {
   sh = 0.5f * (e - r);
   ch = 0.5f * (e + r);
 }
-__device__ __forceinline__ double pos_sqrt(double x) { return fast_sqrt(x > 0.0 ? x : 0.0); }
+__device__ __forceinline__ double pos_sqrt(double x) { return fast_sqrt(x); }  // x < 0 -> 0
 __device__ __forceinline__ float pos_sqrt(float x) { return fast_sqrt(x > 0.f ? x : 0.f); }
 
 // CM-frame mass of a PtEtaPhiM pair (fast domain), computed in coordinates
@@ -481,9 +507,9 @@ __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1,
   sinh_cosh(eta1, sh1, ch1);
   sinh_cosh(eta2, sh2, ch2);
   T q1 = pt1 * ch1, q2 = pt2 * ch2;
-  V4<T> a{pt1, T(0), pt1 * sh1, pos_sqrt(m1 * (m1 < T(0) ? -m1 : m1) + q1 * q1)};
-  V4<T> b{pt2 * cd, pt2 * sd, pt2 * sh2, pos_sqrt(m2 * (m2 < T(0) ? -m2 : m2) + q2 * q2)};
-  T M = cm_pair_mass(a, b, a_out, b_out);
+  V4<T> a{pt1, T(0), pt1 * sh1, pos_sqrt(m1 * fabs(m1) + q1 * q1)};
+  V4<T> b{pt2 * cd, pt2 * sd, pt2 * sh2, pos_sqrt(m2 * fabs(m2) + q2 * q2)};
+  T M = cm_pair_mass<T, true>(a, b, a_out, b_out);
   if (a_out) {
     T s1, c1;
     fast_sincos(phi1, s1, c1);
@@ -552,28 +578,58 @@ __device__ __forceinline__ T pair_mass_ptetaphie(T pt1, T eta1, T phi1, T E1, T 
 
 // ---------------------------------------------------------------------------
 // ROOT FindFixBin in double, bit-identical to the oracle's
-//   1 + (int)((nbins * (x - lo)) / (hi - lo))
-// The quotient is first formed with a precomputed reciprocal (error a few
-// ulp); only when it lies within 1e-14 (relative) of an integer — where the
-// rounding of the exact IEEE division could change the truncation — is the
-// IEEE division evaluated, so the bin equals the oracle's for equal x.
+//   x < lo -> 0;  !(x < hi) -> nbins+1;  else 1 + (int)((nbins * (x - lo)) / (hi - lo))
+// Fast path (5 FP64 ops, the rest on the integer pipe): q = (x - lo) * scale,
+// scale = nbins / (hi - lo), is within 4 ulp of the oracle's quotient (2u
+// relative on each side), so floor(q) equals the oracle's truncation unless q
+// lies within 1e-14 * nbins of an integer. k = rint(q) comes from the
+// 1.5*2^52 shifter; d = q - k is exact (Sterbenz). When t = q + MAGIC has the
+// high word 0x43380000 and k <= nbins, q is in [-0.5, nbins + 0.5) and the bin
+// is 1 + k - (d < 0) (k = 0, d < 0 -> 0 = underflow; k = nbins, d >= 0 ->
+// nbins+1 = overflow, both exactly the oracle's x < lo / !(x < hi) once
+// |d| > tol). Outside that window the sign of q decides (x < lo - w/2 or
+// x > hi + w/2). Near-integer q and non-finite x (NaN -> overflow) take the
+// literal definition out of line.
 // ---------------------------------------------------------------------------
 struct HistParams {
-  double lo, hi, width, inv_width;  // width = hi - lo (same IEEE value the oracle forms)
-  double nbins_d;                   // (double)nbins
+  double lo, hi, width;  // width = hi - lo (the same IEEE value the oracle forms)
+  double nbins_d;        // (double)nbins
+  double scale;          // nbins_d / width
   int nbins;
+  uint32_t near_hi;      // high word of 1e-14 * nbins: |d| with abs_hi(d) <= near_hi is "near"
 };
 
-__device__ __forceinline__ int find_bin(double x, const HistParams& hp) {
+inline HistParams make_hist_params(double lo, double hi, int nbins) {
+  HistParams hp;
+  hp.lo = lo;
+  hp.hi = hi;
+  hp.width = hi - lo;
+  hp.nbins_d = (double)nbins;
+  hp.scale = hp.nbins_d / hp.width;
+  hp.nbins = nbins;
+  double tol = 1e-14 * hp.nbins_d;
+  uint64_t bits;
+  memcpy(&bits, &tol, 8);
+  hp.near_hi = (uint32_t)(bits >> 32);
+  return hp;
+}
+
+__device__ __noinline__ int find_bin_exact(double x, const HistParams& hp) {
   if (x < hp.lo) return 0;
   if (!(x < hp.hi)) return hp.nbins + 1;
-  double a = __dmul_rn(hp.nbins_d, __dsub_rn(x, hp.lo));
-  double q = a * hp.inv_width;
-  int qi;
-  double qr = rint_shift(q, qi);
-  if (fabs(q - qr) <= q * 1e-14 + 1e-300) return 1 + __double2int_rz(__ddiv_rn(a, hp.width));
-  // q is not within 1e-14 of an integer, so floor(q) = floor(a / width)
-  return 1 + qi - (qr > q ? 1 : 0);
+  return 1 + __double2int_rz(__ddiv_rn(__dmul_rn(hp.nbins_d, __dsub_rn(x, hp.lo)), hp.width));
+}
+
+__device__ __forceinline__ int find_bin(double x, const HistParams& hp) {
+  const double MAGIC = 6755399441055744.0;  // 1.5 * 2^52
+  const double q = __dmul_rn(__dsub_rn(x, hp.lo), hp.scale);
+  const double t = __dadd_rn(q, MAGIC);
+  const int k = __double2loint(t);
+  const double d = __dsub_rn(q, __dsub_rn(t, MAGIC));
+  const bool in = (__double2hiint(t) == 0x43380000) & ((unsigned)k <= (unsigned)hp.nbins);
+  int bin = in ? 1 + k - (__double2hiint(d) < 0 ? 1 : 0) : (__double2hiint(q) < 0 ? 0 : hp.nbins + 1);
+  if ((in & (abs_hi(d) <= hp.near_hi)) | (abs_hi(x) >= 0x7FF00000u)) bin = find_bin_exact(x, hp);
+  return bin;
 }
 
 }  // namespace gvx
