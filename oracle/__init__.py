@@ -62,6 +62,9 @@ def _load():
             getattr(lib, f"gvx_ref_mass_histogram_{sfx}").argtypes = [
                 ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                 ctypes.c_int, P, P]
+            getattr(lib, f"gvx_ref_cm_costheta_{sfx}").argtypes = [
+                ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P,
+                ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P]
             f = getattr(lib, f"gvx_ref_dimuon_histogram_{sfx}")
             f.argtypes = [P, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P]
             f.restype = I64
@@ -192,6 +195,28 @@ def mass_histogram(v1, v2, lo: float, hi: float, nbins: int, cm: bool = False,
     getattr(_load(), f"gvx_ref_mass_histogram_{_sfx(v1.dtype)}")(
         _COORDS[coords], _ptr(v1), _ptr(v2), n, lo, hi, nbins, int(bool(cm)), _ptr(bins), _ptr(m))
     return bins, m
+
+
+def cm_costheta(v1, v2, m_axis=(0.25, 300.0, 1000), c_axis=(-1.0, 1.0, 100),
+                coords: str = "ptetaphim", m_bins=None, c_bins=None):
+    """CM decay angle (reading R22): cos θ* = p'1z/|p'1| of vector 1 after
+    the CM boost of reading R11, with the CM mass and cos θ* histograms (reading R12).
+    Returns ``(m_bins, c_bins, M_cm, cos_theta)``; bins accumulate if given."""
+    v1 = _vecs(v1, 4)
+    v2 = _vecs(v2, 4, v1.dtype)
+    if v1.shape != v2.shape:
+        raise ValueError(f"length mismatch: {v1.shape[0]} vs {v2.shape[0]}")
+    n = v1.shape[0]
+    if m_bins is None:
+        m_bins = np.zeros(m_axis[2] + 2, np.uint64)
+    if c_bins is None:
+        c_bins = np.zeros(c_axis[2] + 2, np.uint64)
+    m = np.empty(n, v1.dtype)
+    c = np.empty(n, v1.dtype)
+    getattr(_load(), f"gvx_ref_cm_costheta_{_sfx(v1.dtype)}")(
+        _COORDS[coords], _ptr(v1), _ptr(v2), n, float(m_axis[0]), float(m_axis[1]), int(m_axis[2]),
+        _ptr(m_bins), float(c_axis[0]), float(c_axis[1]), int(c_axis[2]), _ptr(c_bins), _ptr(m), _ptr(c))
+    return m_bins, c_bins, m, c
 
 
 def dimuon_histogram(muons, charge, offsets, lo: float, hi: float, nbins: int, bins=None):

@@ -37,6 +37,10 @@ int32_t gvx_ref_find_bin(double x, double lo, double hi, int32_t nbins);
                                T *elab_out, T *boosted_out);                                      \
     void gvx_ref_mass_histogram_##SFX(int coords, const T *v1, const T *v2, int64_t n, double lo, \
                                       double hi, int32_t nbins, int cm, uint64_t *bins, T *m_out);  \
+    void gvx_ref_cm_costheta_##SFX(int coords, const T *v1, const T *v2, int64_t n, double m_lo,   \
+                                   double m_hi, int32_t m_nbins, uint64_t *m_bins, double c_lo,   \
+                                   double c_hi, int32_t c_nbins, uint64_t *c_bins, T *m_out,      \
+                                   T *cos_out);                                                   \
     int64_t gvx_ref_dimuon_histogram_##SFX(const T *muons, const int32_t *charge,                 \
                                            const int64_t *offsets, int64_t n_events, double lo,   \
                                            double hi, int32_t nbins, uint64_t *bins, T *m_out);

@@ -293,6 +293,40 @@ def test_histogram_single_bin_and_specials(gvx, O):
     assert hg[NB + 1] == 2 and hg[1] == 1
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_find_bin_bit_exact_at_edges(gvx, O, dt):
+    """Reading R12: for identical mass bits the kernel's bin is the oracle's FindBin,
+    also on and within a few ulp of every kind of edge (the GPU's fast binning must
+    send those to the exact division). Masses are fed exactly: PxPyPzE (0,0,0,x) + 0
+    has M = sqrt(x*x) = x, and (p,0,0,0) + 0 has M = -p (both sides IEEE sqrt)."""
+    rng = np.random.default_rng(7)
+    for lo, hi, nb in ((LO, HI, NB), (0.0, 1.0, 10), (-50.0, 50.0, 100_000), (0.1, 0.7, 3), (1e-3, 1e3, 999)):
+        w = (hi - lo) / nb
+        ks = np.unique(np.concatenate([[0, 1, 2, nb - 1, nb], rng.integers(0, nb + 1, 300)]))
+        x = lo + ks * w
+        x = np.concatenate([x, lo + (hi - lo) * ks / nb, [lo, hi, hi + w, lo - w, 2 * hi]]).astype(dt)
+        xs = [x]
+        for s in (1, 2, 3):
+            up, dn = x.copy(), x.copy()
+            for _ in range(s):
+                up = np.nextafter(up, dt(np.inf))
+                dn = np.nextafter(dn, dt(-np.inf))
+            xs += [up, dn]
+        x = np.concatenate(xs + [rng.uniform(lo - w, hi + w, 2000).astype(dt)])
+        x = x[np.isfinite(x) & (np.abs(x) < (1e18 if dt == np.float32 else 1e150))]
+        v1 = np.zeros((x.size + 4, 4), dt)
+        pos = x >= 0
+        v1[:x.size][pos, 3] = x[pos]
+        v1[:x.size][~pos, 0] = -x[~pos]   # M = -|px|
+        v1[x.size:] = np.array([[np.nan, 0, 0, 1], [0, 0, 0, np.inf], [np.inf, 0, 0, 0], [0, 0, 0, 0]], dt)
+        v2 = np.zeros_like(v1)
+        ho, mo = O.mass_histogram(v1, v2, lo, hi, nb, coords="pxpypze")
+        m_out = torch.empty(v1.shape[0], dtype=TDT[dt], device="cuda")
+        hg = host(gvx.mass_histogram(dev(v1), dev(v2), lo, hi, nb, coords="pxpypze", m_out=m_out))
+        assert np.array_equal(host(m_out), mo, equal_nan=True), (lo, hi, nb)
+        assert np.array_equal(hg, ho.astype(np.int64)), (lo, hi, nb, np.nonzero(hg != ho.astype(np.int64))[0][:10])
+
+
 def test_histogram_nbins_variants(gvx, O):
     v1, v2 = synth.muon_pairs(np.arange(50_000), dtype=np.float64)
     for lo, hi, nb in ((0.0, 200.0, 1), (0.0, 200.0, 7), (-50.0, 50.0, 100_000)):

@@ -551,3 +551,106 @@ def test_lorentz_transform_pins(O):
         O.lorentz_transform(v, 2 * np.eye(4))
     with pytest.raises(O.DomainError):
         O.lorentz_transform(v, np.full((4, 4), np.nan))
+
+
+# --------------------------------------------------------------------------
+# CM decay angle cos θ* (reading R22)
+# --------------------------------------------------------------------------
+
+def _rest_frame_decay_in_lab(pstar, theta, phi, m, beta):
+    """Two-body decay at rest (vector 1 at polar angle θ, azimuth φ; vector 2 opposite),
+    then boosted into the lab by β along the rapidity route (mpmath, 40 digits)."""
+    with mp.workdps(40):
+        ps, th, ph, mm = (mp.mpf(x) for x in (pstar, theta, phi, m))
+        E = mp.sqrt(ps * ps + mm * mm)
+        p1 = [ps * mp.sin(th) * mp.cos(ph), ps * mp.sin(th) * mp.sin(ph), ps * mp.cos(th), E]
+        p2 = [-p1[0], -p1[1], -p1[2], E]
+        return [float(x) for x in truth_boost(p1, beta)], [float(x) for x in truth_boost(p2, beta)]
+
+
+def test_costheta_recovers_rest_frame_angle(O):
+    """Closed form: boosting a rest-frame decay by β and then applying the CM path gives back
+    the rest-frame angle, because β_cm = −P/E = −β and two pure boosts along one axis
+    compose to the identity (no Wigner rotation)."""
+    rng = np.random.default_rng(3)
+    rows1, rows2, want, gam = [], [], [], []
+    for _ in range(300):
+        th = rng.uniform(0, np.pi)
+        ph = rng.uniform(-np.pi, np.pi)
+        pstar = rng.uniform(1.0, 60.0)
+        d = rng.normal(size=3)
+        b = 0.99 * rng.uniform() ** (1 / 3) * d / np.linalg.norm(d)
+        a, c = _rest_frame_decay_in_lab(pstar, th, ph, MMU, b)
+        rows1.append(a)
+        rows2.append(c)
+        want.append(math.cos(th))
+        gam.append(1 / math.sqrt(1 - b @ b))
+    v1, v2 = np.array(rows1), np.array(rows2)
+    _, _, m, cos = O.cm_costheta(v1, v2, coords="pxpypze")
+    err = np.abs(cos - np.array(want))
+    # input rounding (1e-16 relative on lab components ~ γE) maps to ~γ² 1e-16 E/p* in cos θ*
+    assert err.max() <= 1e-12, err.max()
+    # swapping the two vectors flips the angle (p2' = −p1' in the CM)
+    _, _, _, cos_sw = O.cm_costheta(v2, v1, coords="pxpypze")
+    assert np.max(np.abs(cos_sw + cos)) <= 1e-12
+    # f32: same pins at the fp32 scale (γ ≤ 7.1 here)
+    _, _, _, c32 = O.cm_costheta(v1.astype(np.float32), v2.astype(np.float32), coords="pxpypze")
+    g = np.array(gam)
+    assert np.all(np.abs(c32.astype(np.float64) - want) <= 2e-5 * g * g)
+
+
+def _truth_costheta(a, b):
+    """cos θ* along the rapidity route: β_cm = −P/E, vector 1 boosted by truth_boost."""
+    with mp.workdps(40):
+        A = [mp.mpf(float(x)) for x in a]
+        B = [mp.mpf(float(x)) for x in b]
+        E = A[3] + B[3]
+        beta = [-(A[k] + B[k]) / E for k in range(3)]
+        p = truth_boost(A, beta)
+        return float(p[2] / mp.sqrt(p[0] ** 2 + p[1] ** 2 + p[2] ** 2)), float(E), float(
+            mp.sqrt(p[0] ** 2 + p[1] ** 2 + p[2] ** 2))
+
+
+@pytest.mark.parametrize("dt,bound", [(np.float64, 1e-13), (np.float32, 5e-6)])
+def test_costheta_random_vs_rapidity_truth(O, dt, bound):
+    v1, v2 = synth.muon_pairs(np.arange(400), seed=31, dtype=dt)
+    _, _, mcm, cos = O.cm_costheta(v1, v2)
+    # truth from the Cartesian inputs the oracle itself forms (the conversion is pinned elsewhere)
+    a = np.array([[x[0] * np.cos(x[2]), x[0] * np.sin(x[2]), x[0] * np.sinh(x[1]),
+                   np.sqrt(x[3] ** 2 + (x[0] * np.cosh(x[1])) ** 2)] for x in v1.astype(np.float64)])
+    b = np.array([[x[0] * np.cos(x[2]), x[0] * np.sin(x[2]), x[0] * np.sinh(x[1]),
+                   np.sqrt(x[3] ** 2 + (x[0] * np.cosh(x[1])) ** 2)] for x in v2.astype(np.float64)])
+    worst = 0.0
+    for i in range(v1.shape[0]):
+        t, E, pstar = _truth_costheta(a[i], b[i])
+        S = E * E / max(float(mcm[i]), 1e-300)  # γ·E scale of the CM boost (as for M_cm)
+        worst = max(worst, abs(float(cos[i]) - t) * pstar / S)
+    assert worst <= bound, worst
+    assert np.all(np.abs(cos.astype(np.float64)) <= 1 + 4 * np.finfo(dt).eps)
+
+
+def test_costheta_degenerate_and_histograms(O):
+    # pair at rest back to back along +z: β = 0, cos θ* = 1 exactly → overflow bin of [−1, 1)
+    a = np.array([[0.0, 0.0, 3.0, 5.0], [4.0, 0.0, 0.0, 5.0], [0.0, 0.0, -3.0, 5.0]])
+    b = np.array([[0.0, 0.0, -3.0, 5.0], [-4.0, 0.0, 0.0, 5.0], [0.0, 0.0, 3.0, 5.0]])
+    mb, cb, m, c = O.cm_costheta(a, b, coords="pxpypze", c_axis=(-1.0, 1.0, 4))
+    assert np.array_equal(c, [1.0, 0.0, -1.0]) and np.array_equal(m, [10.0, 10.0, 10.0])
+    assert cb.tolist() == [0, 1, 0, 1, 0, 1]  # −1 → bin 1, 0 → bin 3, +1 → overflow
+    # zero pair, lightlike collinear pair → NaN (reading R11) → overflow of both axes
+    z = np.zeros((2, 4))
+    z[1] = [0.0, 0.0, 5.0, 5.0]
+    mb, cb, m, c = O.cm_costheta(z, np.array([[0.0] * 4, [0.0, 0.0, 5.0, 5.0]]), coords="pxpypze")
+    assert np.isnan(m).all() and np.isnan(c).all() and mb[-1] == 2 and cb[-1] == 2
+    # the histograms are the bincounts of the per-event values; mass axis == the CM histogram
+    v1, v2 = synth.muon_pairs(np.arange(5000), seed=4, dtype=np.float64)
+    mb, cb, m, c = O.cm_costheta(v1, v2, c_axis=(-1.0, 1.0, 50))
+    ref_m, _ = O.mass_histogram(v1, v2, 0.25, 300.0, 1000, cm=True)
+    assert np.array_equal(mb, ref_m)
+    ref_c = np.zeros(52, np.uint64)
+    for x in c:
+        ref_c[O.find_bin(float(x), -1.0, 1.0, 50)] += 1
+    assert np.array_equal(cb, ref_c)
+    # isotropic-ish sample: both hemispheres populated, accumulation doubles
+    assert cb[1:26].sum() > 1000 and cb[26:51].sum() > 1000
+    mb2, cb2, _, _ = O.cm_costheta(v1, v2, c_axis=(-1.0, 1.0, 50), m_bins=mb.copy(), c_bins=cb.copy())
+    assert np.array_equal(cb2, 2 * cb) and np.array_equal(mb2, 2 * mb)
