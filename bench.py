@@ -388,6 +388,8 @@ def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
         "hist_soa": (lambda: gvx.mass_histogram(s1, s2), 8 * es),
         "boost_uniform": (lambda: gvx.boost_uniform(bv, (0.3, -0.4, 0.5), out=bout), 8 * es),
         "lorentz_4x4": (lambda: gvx.lorentz_transform(bv, LORENTZ_DEMO, out=bout), 8 * es),
+        # f2: CM mass + cos θ* histograms in one pass (reading R22)
+        "cm_costheta_hist": (lambda: gvx.cm_costheta_histogram(v1, v2), 8 * es),
     }
     # jagged events (f4): 1 event per pair slot of the batch, ~1.1 muons/event on average
     import synth.device as sd

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define GVX_ABI_VERSION 2
+#define GVX_ABI_VERSION 3
 
 typedef struct CUstream_st *gvx_stream_t; /* == cudaStream_t */
 
@@ -154,6 +154,31 @@ gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4
                               int32_t nbins, unsigned long long *bins, uint32_t flags,
                               void *m_out, const gvx_vec4_view *boosted_out,
                               gvx_stream_t stream);
+
+/*
+ * gvx_cm_costheta_histogram — CM decay angle ("the CM path's
+ * boosted outputs with a cos theta* histogram"; R22). Each pair is
+ * boosted to its CM frame exactly as gvx_mass_histogram with
+ * GVX_HIST_BOOST_TO_CM does (beta_cm = -(p1+p2)/(E1+E2), lab-parallel axes,
+ * R11), and in ONE pass over the inputs
+ *   the CM mass M goes to the mass axis (m_lo, m_hi, m_nbins -> m_bins) and
+ *   cos theta* = p'1z / |p'1| of boosted vector 1 to the angle axis
+ *   (c_lo, c_hi, c_nbins -> c_bins),
+ * both binned ROOT-style as gvx_mass_histogram (R12; NaN -> overflow, so an
+ * invalid CM boost or |p'1| = 0 lands in both overflow bins; cos theta* = +1
+ * exactly lands in the overflow bin of a [-1, 1) axis).
+ *   m_bins, c_bins  m_nbins+2 / c_nbins+2 uint64 counters (device), ACCUMULATED.
+ *   m_out, cos_out  NULL or n values of dtype (device).
+ * Accuracy: M as the CM histogram; |cos_gpu - cos_exact| <= 2 tau_b S / |p'1|,
+ * S = E_lab^2 / M_lab (the CM boost's gamma E scale), tau_b = 1e-12 (f64) /
+ * 1e-4 (f32, the boosted-vector scale of SURVEY §8(c)).
+ * Errors as gvx_mass_histogram, for either axis.
+ */
+gvx_status gvx_cm_costheta_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview *v1,
+                                     const gvx_vec4_cview *v2, int64_t n, double m_lo, double m_hi,
+                                     int32_t m_nbins, unsigned long long *m_bins, double c_lo,
+                                     double c_hi, int32_t c_nbins, unsigned long long *c_bins,
+                                     void *m_out, void *cos_out, gvx_stream_t stream);
 
 /*
  * gvx_dimuon_histogram — jagged, RDataFrame-style events (PAPER.md:366 names

@@ -43,7 +43,7 @@ GVX_PXPYPZE = 1
 GVX_PXPYPZM = 2
 GVX_PTETAPHIE = 3
 GVX_HIST_BOOST_TO_CM = 0x1
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # The default histogram of the north star: 1000 bins over the dimuon range
 # (reading R13).
@@ -100,6 +100,10 @@ def _load_lib():
     lib.gvx_dimuon_histogram.argtypes = [st, ctypes.POINTER(Vec4CView), P, P, I64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_int32, P, P, P]
     lib.gvx_dimuon_histogram.restype = st
+    lib.gvx_cm_costheta_histogram.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
+                                              ctypes.c_double, ctypes.c_double, ctypes.c_int32, P,
+                                              ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P, P]
+    lib.gvx_cm_costheta_histogram.restype = st
     lib.gvx_status_string.argtypes = [st]
     lib.gvx_status_string.restype = ctypes.c_char_p
     lib.gvx_last_cuda_error_string.argtypes = []
@@ -315,6 +319,51 @@ def mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = D
                                       float(lo), float(hi), int(nbins), bins.data_ptr(), flags, mptr, bo_ref,
                                       _stream(dev)), "gvx_mass_histogram")
     return bins
+
+
+def _out_1d(t: Optional[torch.Tensor], n: int, dt, name: str):
+    if t is None:
+        return None
+    _require_cuda(t, name)
+    if t.shape != (n,) or t.dtype != dt or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous [N] tensor of the inputs' dtype")
+    return t.data_ptr()
+
+
+def _bins_arg(bins: Optional[torch.Tensor], nbins: int, dev, name: str) -> torch.Tensor:
+    if bins is None:
+        bins = new_bins(nbins, dev)
+    _require_cuda(bins, name)
+    if bins.shape != (nbins + 2,) or bins.dtype != torch.int64 or not bins.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous int64 tensor of shape [{nbins + 2}]")
+    return bins
+
+
+def cm_costheta_histogram(v1: VecArg, v2: VecArg, m_axis=(DEFAULT_LO, DEFAULT_HI, DEFAULT_NBINS),
+                          c_axis=(-1.0, 1.0, 100), m_bins: Optional[torch.Tensor] = None,
+                          c_bins: Optional[torch.Tensor] = None, m_out: Optional[torch.Tensor] = None,
+                          cos_out: Optional[torch.Tensor] = None, coords: str = "ptetaphim"):
+    """CM decay angle (DESIGN R22): boost each pair to its CM frame, then bin the CM mass on
+    ``m_axis`` and cos θ* = p'1z/|p'1| on ``c_axis`` (each ``(lo, hi, nbins)``) in one pass.
+    Returns ``(m_bins, c_bins)`` ([nbins+2] int64 each, accumulated)."""
+    a, n, dt, dev, _ = _view(v1, 4, "v1")
+    b, n2, dt2, dev2, _ = _view(v2, 4, "v2")
+    if n != n2:
+        raise ValueError(f"length mismatch: v1 has {n} vectors, v2 has {n2}")
+    if dt != dt2 or dev != dev2:
+        raise ValueError("v1 and v2 must share dtype and device")
+    m_lo, m_hi, m_nb = float(m_axis[0]), float(m_axis[1]), int(m_axis[2])
+    c_lo, c_hi, c_nb = float(c_axis[0]), float(c_axis[1]), int(c_axis[2])
+    m_bins = _bins_arg(m_bins, m_nb, dev, "m_bins")
+    c_bins = _bins_arg(c_bins, c_nb, dev, "c_bins")
+    mptr = _out_1d(m_out, n, dt, "m_out")
+    cptr = _out_1d(cos_out, n, dt, "cos_out")
+    with torch.cuda.device(dev):
+        _check(lib.gvx_cm_costheta_histogram(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b),
+                                             n, m_lo, m_hi, m_nb, m_bins.data_ptr(), c_lo, c_hi, c_nb,
+                                             c_bins.data_ptr(), mptr, cptr, _stream(dev)),
+               "gvx_cm_costheta_histogram")
+    return m_bins, c_bins
 
 
 def dimuon_histogram(muons: VecArg, charge: torch.Tensor, offsets: torch.Tensor, lo: float = DEFAULT_LO,

@@ -179,8 +179,10 @@ bool tma_preferred() {
 template <typename T, int MODE> struct TmaCfgOf;
 template <int MODE> struct TmaCfgOf<double, MODE> { using type = PairTma<double, 896, 2, 28, 1>; };
 template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 992, 3, 31, 1>; };
+template <> struct TmaCfgOf<double, PM_HIST_CM_COS> { using type = PairTma<double, 992, 3, 31, 1>; };
 template <int MODE> struct TmaCfgOf<float, MODE> { using type = PairTma<float, 896, 4, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM> { using type = PairTma<float, 1792, 3, 28, 1>; };
+template <> struct TmaCfgOf<float, PM_HIST_CM_COS> { using type = PairTma<float, 1792, 3, 28, 1>; };
 
 #ifdef GVX_TUNE
 // Tuning build only (tools/libgvx_tune.so): GVX_TMA_CFG / GVX_LDG_CFG pick
@@ -197,11 +199,11 @@ int tune_env(const char* name) {
 template <typename T, int C, int MODE, typename CFG>
 gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, void* m_out,
                                const HistParams& hp, unsigned long long* bins, const gvx_vec4_view* bo,
-                               cudaStream_t s) {
+                               cudaStream_t s, const CosOut<T>& co = CosOut<T>{}) {
   // AoS (paper layout) or SoA with 16-byte aligned component arrays; else not handled here.
   const bool soa = classify(v1, sizeof(T)) == L_SOA && classify(v2, sizeof(T)) == L_SOA;
   if (!soa && !(classify(v1, sizeof(T)) == L_AOS && classify(v2, sizeof(T)) == L_AOS)) return GVX_ERR_UNSUPPORTED;
-  const int nbs = MODE == PM_MASS ? 0 : hp.nbins + 2;
+  const int nbs = MODE == PM_MASS ? 0 : hp.nbins + 2 + (MODE == PM_HIST_CM_COS ? co.hc.nbins + 2 : 0);
   const size_t sm = CFG::smem_bytes(nbs);
   if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
   auto k = soa ? k_pair_tma<T, C, MODE, CFG, false, true> : k_pair_tma<T, C, MODE, CFG, false, false>;
@@ -224,7 +226,9 @@ gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v
       a.c[c] += off * a.s;
       b.c[c] += off * b.s;
     }
-    k<<<grid, block, sm, s>>>(a, b, cn, m_out ? (T*)m_out + off : nullptr, hp, bins, bo2);
+    CosOut<T> co2 = co;
+    if (co2.cos_out) co2.cos_out += off;
+    k<<<grid, block, sm, s>>>(a, b, cn, m_out ? (T*)m_out + off : nullptr, hp, bins, bo2, co2);
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GVX_OK : cuda_fail(e);
@@ -232,7 +236,10 @@ gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v
 
 template <typename T, int C, int MODE>
 gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, void* m_out,
-                           const HistParams& hp, unsigned long long* bins, const gvx_vec4_view* bo, cudaStream_t s) {
+                           const HistParams& hp, unsigned long long* bins, const gvx_vec4_view* bo, cudaStream_t s,
+                           const CosOut<T>& co = CosOut<T>{}) {
+  if constexpr (MODE == PM_HIST_CM_COS)
+    return launch_pair_tma_cfg<T, C, MODE, typename TmaCfgOf<T, MODE>::type>(v1, v2, n, m_out, hp, bins, bo, s, co);
 #ifdef GVX_TUNE
   if constexpr (sizeof(T) == 8 && C == C_PTETAPHIM) {
     switch (tune_env("GVX_TMA_CFG")) {
@@ -406,6 +413,45 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
   if (L == L_AOS) return launch_hist<T, C, L_AOS, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
   if (L == L_SOA) return launch_hist<T, C, L_SOA, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
   return launch_hist<T, C, L_GEN, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
+}
+
+// ------------------------------------------------------ cos theta* -------
+template <typename T, int C>
+gvx_status dispatch_costheta(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, const HistParams& hm,
+                             unsigned long long* mbins, const HistParams& hc, unsigned long long* cbins, void* m_out,
+                             void* cos_out, cudaStream_t s) {
+  const int l1 = classify(v1, sizeof(T)), l2 = classify(v2, sizeof(T));
+  CosOut<T> co{hc, cbins, (T*)cos_out};
+  if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
+    if (((l1 == L_AOS && l2 == L_AOS) || (l1 == L_SOA && l2 == L_SOA)) && tma_enabled()) {
+      gvx_status st = launch_pair_tma<T, C, PM_HIST_CM_COS>(v1, v2, n, m_out, hm, mbins, nullptr, s, co);
+      if (st != GVX_ERR_UNSUPPORTED) return st;
+    }
+  }
+  const size_t nb = (size_t)hm.nbins + 2 + (size_t)hc.nbins + 2;
+  cudaError_t e;
+  if (nb <= kMaxSmemBins) {
+    auto k = k_cm_costheta<T, C, true>;
+    const size_t sm = nb * sizeof(unsigned int);
+    const int grid = grid_for(k, kBlock, sm, kBlock, n);
+    const int64_t chunk = (int64_t)grid << 31;  // uint32 shared-memory counters
+    for (int64_t off = 0; off < n; off += chunk) {
+      const int64_t cn = n - off < chunk ? n - off : chunk;
+      View4<T> a = mk4<T>(v1), b = mk4<T>(v2);
+      for (int c = 0; c < 4; ++c) {
+        a.c[c] += off * a.s;
+        b.c[c] += off * b.s;
+      }
+      k<<<grid, kBlock, sm, s>>>(a, b, cn, hm, mbins, hc, cbins, m_out ? (T*)m_out + off : nullptr,
+                                 cos_out ? (T*)cos_out + off : nullptr);
+    }
+  } else {
+    auto k = k_cm_costheta<T, C, false>;
+    k<<<grid_for(k, kBlock, 0, kBlock, n), kBlock, 0, s>>>(mk4<T>(v1), mk4<T>(v2), n, hm, mbins, hc, cbins,
+                                                           (T*)m_out, (T*)cos_out);
+  }
+  e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
 }
 
 // ---------------------------------------------------------- lorentz ------
@@ -602,6 +648,37 @@ gvx_status gvx_boost_uniform(gvx_dtype dtype, const gvx_vec4_cview* v, double bx
   if (!view_ok<4>(v, es) || !out_view_ok(out, es)) return GVX_ERR_INVALID_ARGUMENT;
   if (dtype == GVX_F64) return launch_boost<double, true>(v, nullptr, out, n, bx, by, bz, s);
   return launch_boost<float, true>(v, nullptr, out, n, (float)bx, (float)by, (float)bz, s);
+}
+
+gvx_status gvx_cm_costheta_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,
+                                     const gvx_vec4_cview* v2, int64_t n, double m_lo, double m_hi, int32_t m_nbins,
+                                     unsigned long long* m_bins, double c_lo, double c_hi, int32_t c_nbins,
+                                     unsigned long long* c_bins, void* m_out, void* cos_out, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || !valid_coords(coords) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (m_nbins < 1 || m_nbins > (1 << 28) || !isfinite(m_lo) || !isfinite(m_hi) || !(m_lo < m_hi))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if (c_nbins < 1 || c_nbins > (1 << 28) || !isfinite(c_lo) || !isfinite(c_hi) || !(c_lo < c_hi))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GVX_OK;
+  const size_t es = dsize(dtype);
+  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !m_bins || !aligned(m_bins, 8) || !c_bins ||
+      !aligned(c_bins, 8))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if ((m_out && !aligned(m_out, es)) || (cos_out && !aligned(cos_out, es))) return GVX_ERR_INVALID_ARGUMENT;
+  const HistParams hm = make_hist_params(m_lo, m_hi, m_nbins), hc = make_hist_params(c_lo, c_hi, c_nbins);
+  cudaStream_t s = (cudaStream_t)stream;
+#define GVX_COS_COORDS(T)                                                                                    \
+  switch (coords) {                                                                                         \
+    case GVX_PTETAPHIM: return dispatch_costheta<T, C_PTETAPHIM>(v1, v2, n, hm, m_bins, hc, c_bins, m_out, cos_out, s); \
+    case GVX_PXPYPZE: return dispatch_costheta<T, C_PXPYPZE>(v1, v2, n, hm, m_bins, hc, c_bins, m_out, cos_out, s);     \
+    case GVX_PXPYPZM: return dispatch_costheta<T, C_PXPYPZM>(v1, v2, n, hm, m_bins, hc, c_bins, m_out, cos_out, s);     \
+    default: return dispatch_costheta<T, C_PTETAPHIE>(v1, v2, n, hm, m_bins, hc, c_bins, m_out, cos_out, s);            \
+  }
+  if (dtype == GVX_F64) {
+    GVX_COS_COORDS(double)
+  }
+  GVX_COS_COORDS(float)
+#undef GVX_COS_COORDS
 }
 
 gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1, const gvx_vec4_cview* v2,

@@ -247,18 +247,23 @@ __global__ void __launch_bounds__(256) k_lorentz(View4<T> v, View4o<T> out, int6
 // ============================================================================
 // K3: fused mass (lab or CM frame) + histogram, privatised in shared memory.
 // ============================================================================
-template <typename T, int COORDS, bool CM, bool WANT_BO = false>
-__device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], int64_t i, const View4o<T>& bo) {
+// WANT_COS (CM only): also cos theta* of boosted vector 1 into *cos (reading R22).
+template <typename T, int COORDS, bool CM, bool WANT_BO = false, bool WANT_COS = false>
+__device__ __forceinline__ T hist_event_mass(const T (&a)[4], const T (&b)[4], int64_t i, const View4o<T>& bo,
+                                             T* cos = nullptr) {
   if constexpr (CM) {
     V4<T> xa, yb;
     T M;
     if (COORDS == C_PTETAPHIM && fast_domain(a[0], a[1], a[2], a[3]) && fast_domain(b[0], b[1], b[2], b[3])) {
-      M = cm_mass_ptetaphim_fast(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3], WANT_BO ? &xa : nullptr, &yb);
+      M = cm_mass_ptetaphim_fast<T, WANT_COS>(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3],
+                                             WANT_BO ? &xa : nullptr, &yb, cos);
     } else if constexpr (COORDS == C_PTETAPHIM) {  // cold path: literal libm conversion
-      M = cm_pair_mass(ptetaphim_exact(a[0], a[1], a[2], a[3]), ptetaphim_exact(b[0], b[1], b[2], b[3]),
-                       WANT_BO ? &xa : nullptr, &yb);
+      M = cm_pair_mass<T, false, WANT_COS>(ptetaphim_exact(a[0], a[1], a[2], a[3]),
+                                           ptetaphim_exact(b[0], b[1], b[2], b[3]), WANT_BO ? &xa : nullptr, &yb,
+                                           cos);
     } else {
-      M = cm_pair_mass(to_cartesian<T, COORDS>(a), to_cartesian<T, COORDS>(b), WANT_BO ? &xa : nullptr, &yb);
+      M = cm_pair_mass<T, false, WANT_COS>(to_cartesian<T, COORDS>(a), to_cartesian<T, COORDS>(b),
+                                           WANT_BO ? &xa : nullptr, &yb, cos);
     }
     if constexpr (WANT_BO) {
       int64_t j0 = (2 * i) * bo.s, j1 = (2 * i + 1) * bo.s;
@@ -320,6 +325,50 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
     for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
       unsigned int c = sh[b];
       if (c) atomicAdd(&bins[b], (unsigned long long)c);
+    }
+  }
+}
+
+// ============================================================================
+// CM mass + cos theta* histograms (reading R22), any layout / coordinates:
+// one event per thread, grid-stride, scalar loads through the views. The
+// AoS / SoA PtEtaPhiM / PxPyPzE fast path is k_pair_tma (PM_HIST_CM_COS).
+// SMEM: both histograms privatised in shared memory (else global atomics).
+// ============================================================================
+template <typename T, int COORDS, bool SMEM>
+__global__ void __launch_bounds__(256) k_cm_costheta(View4<T> v1, View4<T> v2, int64_t n, HistParams hm,
+                                                     unsigned long long* __restrict__ mbins, HistParams hc,
+                                                     unsigned long long* __restrict__ cbins, T* __restrict__ m_out,
+                                                     T* __restrict__ cos_out) {
+  extern __shared__ unsigned int shc[];
+  const int nm = hm.nbins + 2, nc = hc.nbins + 2;
+  if constexpr (SMEM) {
+    for (int b = threadIdx.x; b < nm + nc; b += blockDim.x) shc[b] = 0u;
+    __syncthreads();
+  }
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  View4o<T> none{};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthr) {
+    T x[4], y[4], c;
+    load_event(v1, i, x);
+    load_event(v2, i, y);
+    T M = hist_event_mass<T, COORDS, true, false, true>(x, y, i, none, &c);
+    const int bm = find_bin((double)M, hm), bc = find_bin((double)c, hc);
+    if constexpr (SMEM) {
+      atomicAdd(&shc[bm], 1u);
+      atomicAdd(&shc[nm + bc], 1u);
+    } else {
+      atomicAdd(&mbins[bm], 1ull);
+      atomicAdd(&cbins[bc], 1ull);
+    }
+    if (m_out) m_out[i] = M;
+    if (cos_out) cos_out[i] = c;
+  }
+  if constexpr (SMEM) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < nm + nc; b += blockDim.x) {
+      unsigned int v = shc[b];
+      if (v) atomicAdd(b < nm ? &mbins[b] : &cbins[b - nm], (unsigned long long)v);
     }
   }
 }
@@ -565,7 +614,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
 // HBM reads for later stages stay in flight while the FP64 pipe works —
 // bytes in flight are set by STAGES x TILE, not by register occupancy.
 // ============================================================================
-enum PairMode { PM_MASS = 0, PM_HIST = 1, PM_HIST_CM = 2 };
+enum PairMode { PM_MASS = 0, PM_HIST = 1, PM_HIST_CM = 2, PM_HIST_CM_COS = 3 };
 
 template <typename T, int TILE_, int STAGES_, int NCW_, int MINB_ = 1>
 struct PairTma {
@@ -594,11 +643,26 @@ __device__ __forceinline__ void lds_vec(const float* base, int e, int, float (&x
   x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
 }
 
+// Extra outputs of the cos theta* mode (PM_HIST_CM_COS, reading R22).
+template <typename T> struct CosOut {
+  HistParams hc;          // the angle axis
+  unsigned long long* bins;
+  T* cos_out;             // NULL or n values
+};
+
 template <typename T, int COORDS, int MODE, bool WANT_BO>
 __device__ __forceinline__ void pair_consume(const T (&a)[4], const T (&b)[4], int64_t i, T* __restrict__ m_out,
-                                             unsigned int* sh_hist, const HistParams& hp, const View4o<T>& bo) {
+                                             unsigned int* sh_hist, const HistParams& hp, const View4o<T>& bo,
+                                             unsigned int* sh_cos, const CosOut<T>& co) {
   if constexpr (MODE == PM_MASS) {
     m_out[i] = event_mass<T, COORDS>(a, b);
+  } else if constexpr (MODE == PM_HIST_CM_COS) {
+    T c;
+    T M = hist_event_mass<T, COORDS, true, WANT_BO, true>(a, b, i, bo, &c);
+    atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+    atomicAdd(&sh_cos[find_bin((double)c, co.hc)], 1u);
+    if (m_out) m_out[i] = M;
+    if (co.cos_out) co.cos_out[i] = c;
   } else {
     T M = hist_event_mass<T, COORDS, MODE == PM_HIST_CM, WANT_BO>(a, b, i, bo);
     atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
@@ -612,7 +676,8 @@ __device__ __forceinline__ void pair_consume(const T (&a)[4], const T (&b)[4], i
 template <typename T, int COORDS, int MODE, typename CFG, bool WANT_BO = false, bool SOA = false>
 __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(View4<T> v1, View4<T> v2,
                                                                  int64_t n, T* __restrict__ m_out, HistParams hp,
-                                                                 unsigned long long* __restrict__ bins, View4o<T> bo) {
+                                                                 unsigned long long* __restrict__ bins, View4o<T> bo,
+                                                                 CosOut<T> co) {
   extern __shared__ __align__(128) unsigned char smem[];
   T* ring = reinterpret_cast<T*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CFG::RING_BYTES);
@@ -620,9 +685,12 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
   unsigned int* sh_hist = reinterpret_cast<unsigned int*>(smem + CFG::RING_BYTES + CFG::BAR_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb2 = hp.nbins + 2;
+  // cos theta* mode: the angle histogram follows the mass histogram in shared memory
+  const int nbt = nb2 + (MODE == PM_HIST_CM_COS ? co.hc.nbins + 2 : 0);
+  unsigned int* sh_cos = sh_hist + nb2;
 
   if constexpr (MODE != PM_MASS) {
-    for (int b = threadIdx.x; b < nb2; b += blockDim.x) sh_hist[b] = 0u;
+    for (int b = threadIdx.x; b < nbt; b += blockDim.x) sh_hist[b] = 0u;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < CFG::STAGES; ++s) {
@@ -700,7 +768,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
 #pragma unroll
       for (int u = 0; u < CFG::EPT; ++u)
         pair_consume<T, COORDS, MODE, WANT_BO>(a[u], b[u], t * CFG::TILE + u * CFG::NCT + ctid, m_out, sh_hist, hp,
-                                               bo);
+                                               bo, sh_cos, co);
       if (++s == CFG::STAGES) { s = 0; ph ^= 1u; }
     }
     // ragged tail (< TILE events): the last CTA, plain loads
@@ -714,15 +782,15 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
 #pragma unroll
           for (int c = 0; c < 4; ++c) { a[c] = v1.c[0][4 * i + c]; b[c] = v2.c[0][4 * i + c]; }
         }
-        pair_consume<T, COORDS, MODE, WANT_BO>(a, b, i, m_out, sh_hist, hp, bo);
+        pair_consume<T, COORDS, MODE, WANT_BO>(a, b, i, m_out, sh_hist, hp, bo, sh_cos, co);
       }
     }
   }
   if constexpr (MODE != PM_MASS) {
     __syncthreads();
-    for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
+    for (int b = threadIdx.x; b < nbt; b += blockDim.x) {
       unsigned int c = sh_hist[b];
-      if (c) atomicAdd(&bins[b], (unsigned long long)c);
+      if (c) atomicAdd(b < nb2 ? &bins[b] : &co.bins[b - nb2], (unsigned long long)c);
     }
   }
 }

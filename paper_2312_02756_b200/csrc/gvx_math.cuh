@@ -467,8 +467,22 @@ __device__ __forceinline__ float fast_signed_sqrt(float m2) {
 __device__ __forceinline__ bool is_positive(double x) { return __double2hiint(x) > 0; }  // x >= 2^-1022 (or +NaN)
 __device__ __forceinline__ bool is_positive(float x) { return x > 0.f; }
 
-template <typename T, bool A_Y0 = false>
-__device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>* a_out, V4<T>* b_out) {
+// cos of the polar angle of v's momentum, p_z / |p| (reading R22); |p| = 0 -> NaN.
+__device__ __forceinline__ double cos_polar(const V4<double>& v) {
+  return v.z * fast_rsqrt(fma(v.x, v.x, fma(v.y, v.y, v.z * v.z)));
+}
+__device__ __forceinline__ float cos_polar(const V4<float>& v) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaf(v.x, v.x, fmaf(v.y, v.y, v.z * v.z))));
+  return v.z * r;
+}
+
+// WANT_COS: also cos theta* of boosted vector 1 (reading R22). The rotated
+// frame of cm_mass_ptetaphim_fast turns about z, which leaves p_z and |p|
+// unchanged, so cos theta* is read before any rotation back.
+template <typename T, bool A_Y0 = false, bool WANT_COS = false>
+__device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>* a_out, V4<T>* b_out,
+                                          T* cos_out = nullptr) {
   T Px = a.x + b.x, Py = a.y + b.y, Pz = a.z + b.z, E = a.t + b.t;
   T inv = any_rcp(E);
   BoostCoef<T> k = boost_coef_fast(-Px * inv, -Py * inv, -Pz * inv);
@@ -478,6 +492,7 @@ __device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>*
   k.ok = true;
   V4<T> a2 = apply_boost<T, A_Y0>(k, a), b2 = apply_boost(k, b);
   if (a_out) { *a_out = a2; *b_out = b2; }
+  if constexpr (WANT_COS) *cos_out = cos_polar(a2);
   T X = a2.x + b2.x, Y = a2.y + b2.y, Z = a2.z + b2.z, W = a2.t + b2.t;
   return fast_signed_sqrt(W * W - (X * X + Y * Y + Z * Z));
 }
@@ -499,9 +514,9 @@ __device__ __forceinline__ float pos_sqrt(float x) { return fast_sqrt(x > 0.f ? 
 // to both vectors literally, but vector 1 becomes (pt1, 0, pt1 sinh eta1, E1)
 // and vector 2 needs only sin/cos of phi2 - phi1 — one sincos per pair instead
 // of two. Boosted vectors, when requested, are rotated back by +phi1.
-template <typename T>
+template <typename T, bool WANT_COS = false>
 __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1, T pt2, T eta2, T phi2, T m2,
-                                                    V4<T>* a_out, V4<T>* b_out) {
+                                                    V4<T>* a_out, V4<T>* b_out, T* cos_out = nullptr) {
   T sd, cd, sh1, ch1, sh2, ch2;
   fast_sincos(phi2 - phi1, sd, cd);
   sinh_cosh(eta1, sh1, ch1);
@@ -509,7 +524,7 @@ __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1,
   T q1 = pt1 * ch1, q2 = pt2 * ch2;
   V4<T> a{pt1, T(0), pt1 * sh1, pos_sqrt(m1 * fabs(m1) + q1 * q1)};
   V4<T> b{pt2 * cd, pt2 * sd, pt2 * sh2, pos_sqrt(m2 * fabs(m2) + q2 * q2)};
-  T M = cm_pair_mass<T, true>(a, b, a_out, b_out);
+  T M = cm_pair_mass<T, true, WANT_COS>(a, b, a_out, b_out, cos_out);
   if (a_out) {
     T s1, c1;
     fast_sincos(phi1, s1, c1);

@@ -74,32 +74,45 @@ def find_bin_np(x, lo, hi, nbins):
 
 
 def hist_check(h_gpu, m_ref, e_lab, tau, lo, hi, nbins, nan_possible=None, m_window_center=None):
-    """Reading R14. Returns a list of failure strings (empty = pass).
+    """Reading R14. Returns ``(failures, n_ambiguous)`` (no failures = pass).
 
     δ_i = τ·E_i² / max(|M_i|, √τ·E_i); event i is ambiguous if an edge of the axis lies
-    within δ_i of its oracle mass M_i. h_s = oracle histogram of non-ambiguous events.
-    Require h_gpu ≥ h_s bin-wise, Σ(h_gpu − h_s) = #ambiguous, and each bin's excess
-    ≤ #ambiguous events whose window [M−δ, M+δ] touches it (events flagged in
-    ``nan_possible`` may also land in the overflow bin; their window is centred on
-    ``m_window_center`` — the lab mass — when the oracle's own mass is NaN)."""
-    h_gpu = np.asarray(h_gpu, np.int64)
+    within δ_i of its oracle mass M_i. Events flagged in ``nan_possible`` may also land in
+    the overflow bin; their window is centred on ``m_window_center`` (the lab mass) when
+    the oracle's own mass is NaN. See hist_check_delta for the rule itself."""
     m = np.asarray(m_ref, np.float64).copy()
     e = np.asarray(e_lab, np.float64)
-    n = m.size
-    nanp = np.zeros(n, bool) if nan_possible is None else np.asarray(nan_possible, bool)
+    nanp = np.zeros(m.size, bool) if nan_possible is None else np.asarray(nan_possible, bool)
     if m_window_center is not None:
         c = np.asarray(m_window_center, np.float64)
         m = np.where(np.isnan(m) & nanp, c, m)
     with np.errstate(invalid="ignore", divide="ignore"):
         delta = tau * e * e / np.maximum(np.abs(m), np.sqrt(tau) * e)
+    return hist_check_delta(h_gpu, m_ref, delta, lo, hi, nbins, nan_possible=nanp, window_center=m)
+
+
+def hist_check_delta(h_gpu, x_ref, delta, lo, hi, nbins, nan_possible=None, window_center=None):
+    """Histogram parity with per-event uncertainty windows [x_i − δ_i, x_i + δ_i] (R14, R22).
+
+    Event i is ambiguous if an edge of the axis lies within δ_i of its oracle value (or it
+    is flagged in ``nan_possible``). h_s = oracle histogram of the non-ambiguous events.
+    Require h_gpu ≥ h_s bin-wise, Σ(h_gpu − h_s) = #ambiguous, and each bin's excess ≤
+    #ambiguous events whose window touches it (nan_possible events may also count in the
+    overflow bin). ``window_center`` replaces x_ref as the window centre where given."""
+    h_gpu = np.asarray(h_gpu, np.int64)
+    x0 = np.asarray(x_ref, np.float64)
+    x = x0 if window_center is None else np.asarray(window_center, np.float64)
+    delta = np.asarray(delta, np.float64)
+    n = x.size
+    nanp = np.zeros(n, bool) if nan_possible is None else np.asarray(nan_possible, bool)
     w = (hi - lo) / nbins
-    fin = np.isfinite(m)
+    fin = np.isfinite(x)
     with np.errstate(invalid="ignore"):
-        k = np.clip(np.round((m - lo) / w), 0, nbins)
+        k = np.clip(np.round((x - lo) / w), 0, nbins)
         nearest_edge = lo + k * w
-        amb = fin & (np.abs(m - nearest_edge) <= delta + 1e-12 * np.abs(m)) & (m > lo - delta - w) & (m < hi + delta + w)
+        amb = fin & (np.abs(x - nearest_edge) <= delta + 1e-12 * np.abs(x)) & (x > lo - delta - w) & (x < hi + delta + w)
     amb |= nanp
-    b_ref = find_bin_np(np.asarray(m_ref, np.float64), lo, hi, nbins)
+    b_ref = find_bin_np(x0, lo, hi, nbins)
     h_s = np.bincount(b_ref[~amb], minlength=nbins + 2).astype(np.int64)
     fails = []
     if (h_gpu < h_s).any():
@@ -109,13 +122,14 @@ def hist_check(h_gpu, m_ref, e_lab, tau, lo, hi, nbins, nan_possible=None, m_win
     if excess.sum() != amb.sum():
         fails.append(f"total excess {excess.sum()} != #ambiguous {amb.sum()}")
     allowed = np.zeros(nbins + 2, np.int64)
-    idx = np.nonzero(amb)[0]
-    for i in idx:
-        if np.isfinite(m[i]):
-            b0 = find_bin_np(m[i] - delta[i], lo, hi, nbins)
-            b1 = find_bin_np(m[i] + delta[i], lo, hi, nbins)
+    for i in np.nonzero(amb)[0]:
+        if np.isfinite(x[i]) and np.isfinite(delta[i]):
+            b0 = find_bin_np(x[i] - delta[i], lo, hi, nbins)
+            b1 = find_bin_np(x[i] + delta[i], lo, hi, nbins)
             allowed[int(b0):int(b1) + 1] += 1
-        if nanp[i] or not np.isfinite(m[i]):
+        elif np.isfinite(x[i]):  # unbounded window: anywhere
+            allowed += 1
+        if nanp[i] or not np.isfinite(x[i]):
             allowed[nbins + 1] += 1
     if (excess > allowed).any():
         bad = np.nonzero(excess > allowed)[0][:10]

@@ -9,7 +9,8 @@ import pytest
 import torch
 
 import synth
-from tests._parity import boost_violations, energy_scale, find_bin_np, hist_check, mass_violations, tau_of
+from tests._parity import (boost_violations, energy_scale, find_bin_np, hist_check, hist_check_delta, mass_violations,
+                           tau_of)
 
 pytestmark = pytest.mark.gpu
 
@@ -731,3 +732,101 @@ def test_dispatch_fuzz(gvx, O):
             else:
                 fails, _ = hist_check(h, mo, e, tau_of(dt), LO, HI, NB)
             assert not fails, (tag, fails)
+
+
+# ----------------------------------------------------------------------------
+# CM decay angle cos θ* (reading R22)
+# ----------------------------------------------------------------------------
+
+def _costheta_reference(O, v1, v2, dt, coords="ptetaphim"):
+    """Oracle cos θ*, its tolerance window δ = 2 τ_b S/|p'1| (S = E_lab²/|M_lab|, the CM
+    boost's γE scale; τ_b = 1e-12 f64, 1e-4 f32 as for the boosted vectors), and the
+    events whose CM boost is ill-conditioned (f32: M_lab/E_lab < 1e-2; any: oracle NaN)."""
+    mb, cb, mo, co = O.cm_costheta(v1, v2, c_axis=(-1.0, 1.0, 100), coords=coords)
+    _, _, bo = O.cm_mass(v1, v2, coords=coords, want_boosted=True)
+    mlab, _ = O.invariant_mass(v1, v2, coords=coords)
+    e = energy_scale(O, v1, v2, coords)
+    tau_b = 1e-12 if dt == np.float64 else 1e-4
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        pstar = np.sqrt((bo[:, :3].astype(np.float64) ** 2).sum(1))
+        S = e * e / np.maximum(np.abs(mlab.astype(np.float64)), 1e-300)
+        delta = 2 * tau_b * S / pstar
+    small = np.abs(mlab.astype(np.float64)) < (1e-2 if dt == np.float32 else 1e-6) * e
+    nanp = np.isnan(co) | np.isnan(mo) | small
+    return mb, cb, mo, co, delta, nanp, mlab, e
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("layout", ["aos", "soa", "pairs"])
+def test_cm_costheta_parity(gvx, O, dt, layout):
+    n = 200_003 if layout == "aos" else 3 * 256 * 148 + 37
+    v1, v2 = mixed_inputs(n, dt, seed=17)
+    mb_o, cb_o, mo, co, delta, nanp, mlab, e = _costheta_reference(O, v1, v2, dt)
+    t1, t2 = dev(v1), dev(v2)
+    if layout == "soa":
+        a = [t1[:, k].contiguous() for k in range(4)]
+        b = [t2[:, k].contiguous() for k in range(4)]
+    elif layout == "pairs":  # interleaved [N][2][4]: the generic strided kernel
+        pr = torch.stack([t1, t2], 1).contiguous()
+        a, b = pr[:, 0], pr[:, 1]
+    else:
+        a, b = t1, t2
+    N = v1.shape[0]
+    m_out = torch.empty(N, dtype=TDT[dt], device="cuda")
+    c_out = torch.empty(N, dtype=TDT[dt], device="cuda")
+    mb, cb = gvx.cm_costheta_histogram(a, b, c_axis=(-1.0, 1.0, 100), m_out=m_out, cos_out=c_out)
+    mb, cb, mg, cg = host(mb), host(cb), host(m_out), host(c_out)
+    assert mb.sum() == N and cb.sum() == N
+    # the mass axis is the CM mass histogram, bit for bit (same arithmetic, same binning)
+    m_ref = torch.empty(N, dtype=TDT[dt], device="cuda")
+    h_cm = host(gvx.mass_histogram(t1, t2, cm=True, m_out=m_ref))
+    assert np.array_equal(mb, h_cm) and np.array_equal(mg, host(m_ref), equal_nan=True)
+    # cos θ* element-wise within the window, class-equal (finite <=> finite) where well conditioned
+    ok = ~nanp
+    c64, g64 = co.astype(np.float64), cg.astype(np.float64)
+    fin = np.isfinite(c64[ok])
+    assert np.array_equal(fin, np.isfinite(g64[ok]))
+    err = np.abs(g64[ok][fin] - c64[ok][fin])
+    assert np.all(err <= delta[ok][fin]), (err / delta[ok][fin]).max()
+    fails, namb = hist_check_delta(cb, co, delta, -1.0, 1.0, 100, nan_possible=nanp)
+    assert not fails, (fails, namb)
+    assert np.abs(g64[np.isfinite(g64)]).max() <= 1 + 1e-6
+
+
+def test_cm_costheta_cartesian_and_closed_form(gvx, O):
+    """PxPyPzE input: rest-frame decays boosted into the lab recover their angle on the GPU too."""
+    rng = np.random.default_rng(11)
+    n = 50_000
+    th = np.arccos(rng.uniform(-1, 1, n))
+    ph = rng.uniform(-np.pi, np.pi, n)
+    ps = rng.uniform(5, 50, n)
+    E = np.sqrt(ps ** 2 + synth.MUON_MASS ** 2)
+    p1 = np.stack([ps * np.sin(th) * np.cos(ph), ps * np.sin(th) * np.sin(ph), ps * np.cos(th), E], 1)
+    p2 = p1 * np.array([-1, -1, -1, 1])
+    d = rng.normal(size=(n, 3))
+    beta = 0.9 * rng.uniform(size=(n, 1)) ** (1 / 3) * d / np.linalg.norm(d, axis=1, keepdims=True)
+    l1, _ = O.boost(p1, beta)
+    l2, _ = O.boost(p2, beta)
+    c_out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _, cb = gvx.cm_costheta_histogram(dev(l1), dev(l2), c_axis=(-1.0, 1.0, 20), cos_out=c_out, coords="pxpypze")
+    assert np.abs(host(c_out) - np.cos(th)).max() <= 1e-11
+    _, cbo, _, co = O.cm_costheta(l1, l2, c_axis=(-1.0, 1.0, 20), coords="pxpypze")
+    assert np.abs(host(c_out) - co).max() <= 1e-12
+    # uniform in cos θ: every one of the 20 bins holds 5 % ± 5σ
+    h = host(cb)[1:21]
+    assert np.all(np.abs(h - n / 20) <= 5 * np.sqrt(n / 20))
+
+
+def test_cm_costheta_errors(gvx):
+    v = torch.zeros((4, 4), dtype=torch.float64, device="cuda")
+    with pytest.raises(gvx.GvxError):
+        gvx.cm_costheta_histogram(v, v, c_axis=(1.0, -1.0, 10))
+    with pytest.raises(gvx.GvxError):
+        gvx.cm_costheta_histogram(v, v, m_axis=(0.0, 1.0, 0))
+    with pytest.raises(ValueError):
+        gvx.cm_costheta_histogram(v, v[:3])
+    mb, cb = gvx.cm_costheta_histogram(v[:0], v[:0])
+    assert int(mb.sum()) == 0 and int(cb.sum()) == 0
+    # zero vectors: invalid CM boost -> both overflow bins
+    mb, cb = gvx.cm_costheta_histogram(v, v, coords="pxpypze", c_axis=(-1.0, 1.0, 10))
+    assert int(mb[-1]) == 4 and int(cb[-1]) == 4
