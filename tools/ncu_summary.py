@@ -32,13 +32,17 @@ METRICS = [
 ]
 
 
-def kernel_key(name: str) -> str:
+def kernel_key(name: str):
+    if "k_boost_inputs" in name or "k_muon_pairs" in name or "k_jagged" in name:
+        return None  # the input generator (synth/), not a hot-path kernel
     if "k_boost" in name:
         return "boost"
     cm = None
     if "k_pair_tma" in name:
         mode = name.split("k_pair_tma<")[1].split(",")[2].strip()
-        return {"0": "invariant_mass", "1": "mass_histogram", "2": "mass_histogram_cm"}[mode]
+        return {"0": "invariant_mass", "1": "mass_histogram", "2": "mass_histogram_cm", "3": "cm_costheta_hist"}[mode]
+    if "k_cm_costheta" in name:
+        return "cm_costheta_hist"
     if "k_invariant_mass" in name:
         return "invariant_mass"
     if "k_mass_histogram" in name:
@@ -51,7 +55,8 @@ def main():
     dtype, rep, rdir = sys.argv[1], sys.argv[2], sys.argv[3]
     n = int(float(sys.argv[4])) if len(sys.argv) > 4 else 100_000_000
     es = 8 if dtype == "f64" else 4
-    algo = {"invariant_mass": 9 * es, "boost": 11 * es, "mass_histogram": 8 * es, "mass_histogram_cm": 8 * es}
+    algo = {"invariant_mass": 9 * es, "boost": 11 * es, "mass_histogram": 8 * es, "mass_histogram_cm": 8 * es,
+            "cm_costheta_hist": 8 * es}
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, units = rows[0], rows[1]
@@ -66,6 +71,8 @@ def main():
             continue
         name = r[h.index("Kernel Name")]
         key = kernel_key(name)
+        if key is None:
+            continue
         vals = []
         for m, _ in METRICS:
             if m in h:

@@ -34,5 +34,6 @@ for _ in range(a.reps):
     gvx.boost(bv, bb, out=out)
     gvx.mass_histogram(v1, v2, bins=bins)
     gvx.mass_histogram(v1, v2, bins=bins, cm=True)
+    gvx.cm_costheta_histogram(v1, v2)
 torch.cuda.synchronize()
 print("prof_step done")
