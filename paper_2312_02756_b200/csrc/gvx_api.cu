@@ -516,6 +516,50 @@ gvx_status launch_dimuon_tma(const gvx_vec4_cview* mu, const int32_t* q, const i
   return e == cudaSuccess ? GVX_OK : cuda_fail(e);
 }
 
+// Stream-compacted dimuon kernel (default): ET events per tile, NT threads.
+// Default geometry from the B200 sweep (profiles/r01/sweep_dimuon_compact.jsonl):
+// 2048-event tiles, 256 threads, 5 CTAs/SM (MINB 5 caps registers at 48).
+template <typename T, bool AOS, int ET = 2048, int NT = 256, int MINB = 5>
+gvx_status launch_dimuon_compact(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
+                                 const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
+#ifdef GVX_TUNE
+  if constexpr (ET == 2048 && NT == 256 && MINB == 5) {
+    switch (tune_env("GVX_DIMUON_CFG")) {
+      case 1: return launch_dimuon_compact<T, AOS, 2048, 256, 4>(mu, q, off, n_events, hp, bins, m_out, s);
+      case 2: return launch_dimuon_compact<T, AOS, 2048, 256, 6>(mu, q, off, n_events, hp, bins, m_out, s);
+      case 3: return launch_dimuon_compact<T, AOS, 1024, 256, 4>(mu, q, off, n_events, hp, bins, m_out, s);
+      case 4: return launch_dimuon_compact<T, AOS, 4096, 256, 4>(mu, q, off, n_events, hp, bins, m_out, s);
+      case 5: return launch_dimuon_compact<T, AOS, 2048, 128, 8>(mu, q, off, n_events, hp, bins, m_out, s);
+      case 6: return launch_dimuon_compact<T, AOS, 4096, 512, 2>(mu, q, off, n_events, hp, bins, m_out, s);
+      default: break;
+    }
+  }
+#endif
+  const size_t sm = dimuon_compact_smem<ET>(hp.nbins + 2);
+  if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
+  auto k = k_dimuon_compact<T, AOS, ET, NT, 1, MINB>;
+  const int grid = grid_for(k, NT, sm, ET, n_events);
+  // uint32 shared-memory bins: one launch covers at most grid * 2^31 events
+  const int64_t chunk = (int64_t)grid << 31;
+  for (int64_t o = 0; o < n_events; o += chunk) {
+    const int64_t cn = n_events - o < chunk ? n_events - o : chunk;
+    k<<<grid, NT, sm, s>>>(mk4<T>(mu), q, off + o, cn, hp, bins, m_out ? (T*)m_out + o : nullptr);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+// GVX_DIMUON_IMPL=tma / ldg selects the streaming kernels for A/B runs.
+int dimuon_impl() {
+  static const int v = [] {
+    const char* e = getenv("GVX_DIMUON_IMPL");
+    if (e && e[0] == 't') return 1;
+    if (e && e[0] == 'l') return 2;
+    return 0;
+  }();
+  return v;
+}
+
 template <typename T>
 gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
                          const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
@@ -524,7 +568,13 @@ gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64
   for (int k = 1; k < 4; ++k) aos = aos && (const char*)mu->c[k] == b + k * sizeof(T);
   const size_t nb2 = (size_t)hp.nbins + 2;
   if (nb2 > kMaxSmemBins) return GVX_ERR_UNSUPPORTED;
-  if (aos && aligned(b, 16) && aligned(off, 16) && aligned(q, 16) && tma_enabled()) {  // TMA column streaming
+  if (dimuon_impl() == 0) {
+    const bool aos_vec = aos && aligned(b, sizeof(T) == 8 ? 32 : 16);  // 256-bit (f64) / 128-bit (f32) muon loads
+    gvx_status st = aos_vec ? launch_dimuon_compact<T, true>(mu, q, off, n_events, hp, bins, m_out, s)
+                            : launch_dimuon_compact<T, false>(mu, q, off, n_events, hp, bins, m_out, s);
+    if (st != GVX_ERR_UNSUPPORTED) return st;
+  }
+  if (dimuon_impl() == 1 && aos && aligned(b, 16) && aligned(off, 16) && aligned(q, 16) && tma_enabled()) {  // TMA column streaming
     gvx_status st = GVX_ERR_UNSUPPORTED;
 #ifdef GVX_TUNE
     switch (tune_env("GVX_DIMUON_CFG")) {

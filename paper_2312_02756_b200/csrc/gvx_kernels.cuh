@@ -452,6 +452,121 @@ __global__ void __launch_bounds__(256) k_dimuon_histogram(View4<T> mu, const int
 }
 
 // ============================================================================
+// Jagged dimuon with stream compaction (default). Only ~15 % of the events
+// of the muon recipe are selected, so a one-lane-per-event kernel runs the
+// mass arithmetic with ~5 of 32 lanes active (the warp pays for all 32) and
+// streams every muon's kinematics although only the selected pairs' are
+// needed. Here a CTA takes a tile of ET events and
+//   1. copies offsets[e0 .. e0+ET] into shared memory (coalesced),
+//   2. selects: count == 2, then the two charges (4-B gathers from a narrow
+//      address range), sign(q0) != sign(q1) (64-bit product: no overflow);
+//      selected events are appended to a shared-memory list with one
+//      warp-aggregated atomic per warp; unselected ones get NaN in m_out,
+//   3. all NT threads walk the compacted list: both muons of U entries are
+//      gathered at once (LDG.256 per f64 muon: memory-level parallelism),
+//      the mass is computed with every lane busy, and binned privately.
+// HBM traffic is the offsets, the charge sectors of 2-muon events and only
+// the selected pairs' kinematics. Several CTAs per SM overlap the phases.
+// ============================================================================
+template <typename T, bool AOS, int ET, int NT, int U = 1, int MINB = 4>
+__global__ void __launch_bounds__(NT, MINB) k_dimuon_compact(View4<T> mu, const int32_t* __restrict__ q,
+                                                        const int64_t* __restrict__ offsets, int64_t n_events,
+                                                        HistParams hp, unsigned long long* __restrict__ bins,
+                                                        T* __restrict__ m_out) {
+  static_assert(ET % NT == 0 && ET <= 65536, "tile geometry");
+  constexpr int EPT = ET / NT;
+  extern __shared__ __align__(128) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);                  // ET + 1 offsets
+  uint16_t* s_list = reinterpret_cast<uint16_t*>(s_off + ET + 2);     // selected event-local indices
+  unsigned int* s_hist = reinterpret_cast<unsigned int*>(s_list + ET);
+  __shared__ int s_n;
+  const int nb2 = hp.nbins + 2;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int b = tid; b < nb2; b += NT) s_hist[b] = 0u;
+  const int64_t ntiles = (n_events + ET - 1) / ET;
+  // Offsets of a tile: EPT+1 loads per thread, all in flight together. The next
+  // tile's are issued before this tile's gather phase (software pipelining), so
+  // their latency hides behind the muon gathers and the mass arithmetic.
+  int64_t r[EPT + 1];
+  auto load_offsets = [&](int64_t tile) {
+    const int64_t e0 = tile * ET;
+    const int ne = (int)(n_events - e0 < ET ? n_events - e0 : ET);
+#pragma unroll
+    for (int k = 0; k <= EPT; ++k) {
+      const int i = tid + k * NT;
+      r[k] = (tile < ntiles && i <= ne) ? __ldg(offsets + e0 + i) : 0;
+    }
+  };
+  load_offsets(blockIdx.x);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t e0 = tile * ET;
+    const int ne = (int)(n_events - e0 < ET ? n_events - e0 : ET);
+    if (tid == 0) s_n = 0;
+#pragma unroll
+    for (int k = 0; k <= EPT; ++k)
+      if (tid + k * NT <= ne) s_off[tid + k * NT] = r[k];
+    __syncthreads();
+    int32_t qa[EPT], qb[EPT];
+    bool two[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {  // all charge gathers of this thread in flight together
+      const int el = tid + k * NT;
+      two[k] = el < ne && s_off[el + 1] - s_off[el] == 2;
+      qa[k] = qb[k] = 0;
+      if (two[k]) {
+        qa[k] = __ldg(q + s_off[el]);
+        qb[k] = __ldg(q + s_off[el] + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int el = tid + k * NT;
+      const bool sel = two[k] && (int64_t)qa[k] * (int64_t)qb[k] < 0;
+      const unsigned int bal = __ballot_sync(0xffffffffu, sel);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&s_n, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (sel) s_list[base + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)el;
+      else if (m_out && el < ne) m_out[e0 + el] = T(NAN);
+    }
+    __syncthreads();
+    const int n = s_n;
+    load_offsets(tile + gridDim.x);
+    for (int j0 = tid; j0 < n; j0 += NT * U) {
+      T a[U][4], b[U][4];
+      int el[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u * NT;
+        el[u] = j < n ? (int)s_list[j] : -1;
+        if (el[u] >= 0) {
+          const int64_t o = s_off[el[u]];
+          load_muon<T, AOS>(mu, o, a[u]);
+          load_muon<T, AOS>(mu, o + 1, b[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (el[u] < 0) break;
+        const T M = event_mass<T, C_PTETAPHIM>(a[u], b[u]);
+        atomicAdd(&s_hist[find_bin((double)M, hp)], 1u);
+        if (m_out) m_out[e0 + el[u]] = M;
+      }
+    }
+    __syncthreads();  // s_off, s_list and s_n are reused by the next tile
+  }
+  for (int b = tid; b < nb2; b += NT) {
+    const unsigned int c = s_hist[b];
+    if (c) atomicAdd(&bins[b], (unsigned long long)c);
+  }
+}
+
+template <int ET>
+constexpr size_t dimuon_compact_smem(int nb2) {
+  return (size_t)(ET + 2) * 8 + (size_t)ET * 2 + (size_t)nb2 * 4;
+}
+
+// ============================================================================
 // Jagged dimuon, TMA-fed: the offsets column and the muon column are streamed
 // tile by tile (ET events per tile) into a shared-memory ring. A tile's muon
 // range [offsets[e0], offsets[e0+ET]) is only known from the offsets, so the

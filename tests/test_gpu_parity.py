@@ -830,3 +830,66 @@ def test_cm_costheta_errors(gvx):
     # zero vectors: invalid CM boost -> both overflow bins
     mb, cb = gvx.cm_costheta_histogram(v, v, coords="pxpypze", c_axis=(-1.0, 1.0, 10))
     assert int(mb[-1]) == 4 and int(cb[-1]) == 4
+
+
+def test_cfg5_costheta_1e9_f32(gvx, O):
+    """cos θ* (R22) at CFG5's per-GPU size, launched as bench.py launches it: 1e9 fp32 pairs.
+    Sampled values vs the oracle; the mass axis equals the CM histogram bit for bit; the
+    angle axis is exactly FindBin of the kernel's own cos θ*; 8-shard accumulation equal."""
+    import synth.device as sd
+    n = 1_000_000_000
+    v1, v2 = sd.muon_pairs(n, dtype=torch.float32)
+    m_out = torch.empty(n, dtype=torch.float32, device="cuda")
+    c_out = torch.empty(n, dtype=torch.float32, device="cuda")
+    mb, cb = gvx.cm_costheta_histogram(v1, v2, m_out=m_out, cos_out=c_out)
+    assert int(mb.sum()) == n and int(cb.sum()) == n
+    assert torch.equal(mb, gvx.mass_histogram(v1, v2, cm=True))
+    x = c_out.double()
+    q = (100.0 * (x + 1.0)) / 2.0
+    inner = 1 + torch.trunc(torch.nan_to_num(q, nan=0.0, posinf=0.0, neginf=0.0)).long()
+    b = torch.where(x < -1.0, 0, torch.where(~(x < 1.0), 101, inner))
+    assert torch.equal(torch.bincount(b, minlength=102), cb)
+    del x, q, inner, b
+    am, ac = gvx.new_bins(), gvx.new_bins(100)
+    for r in range(8):
+        lo, hi = synth.shard_range(n, r, 8)
+        gvx.cm_costheta_histogram(v1[lo:hi], v2[lo:hi], m_bins=am, c_bins=ac)
+    assert torch.equal(am, mb) and torch.equal(ac, cb)
+    idx = _sample_idx(n, seed=5)
+    a, bb = synth.muon_pairs(idx, dtype=np.float32)
+    _, _, mo, co, delta, nanp, _, _ = _costheta_reference(O, a, bb, np.float32)
+    sel = torch.from_numpy(idx).cuda()
+    cg = host(c_out[sel]).astype(np.float64)
+    ok = ~nanp & np.isfinite(co)
+    assert np.all(np.abs(cg[ok] - co[ok]) <= delta[ok])
+
+
+def test_dimuon_1e8_full_size(gvx, O):
+    """Jagged dimuon (f4) at the bench size (1e8 events, f64), launched as bench.py does:
+    the selected count equals the selection rule evaluated by torch on the device columns,
+    the bins are FindBin of the kernel's own masses, sampled events match the oracle."""
+    import synth.device as sd
+    n = 100_000_000
+    mu, q, off = sd.jagged_events(0, n, dtype=torch.float64)
+    m_out = torch.empty(n, dtype=torch.float64, device="cuda")
+    h = gvx.dimuon_histogram(mu, q, off, m_out=m_out)
+    k = off[1:] - off[:-1]
+    first = off[:-1].clamp(max=q.numel() - 2)
+    sel = (k == 2) & (q[first].long() * q[first + 1].long() < 0)
+    assert int(h.sum()) == int(sel.sum())
+    assert torch.equal(torch.isnan(m_out), ~sel)
+    x = m_out.double()
+    qq = (float(NB) * (x - LO)) / (HI - LO)
+    inner = 1 + torch.trunc(torch.nan_to_num(qq, nan=0.0, posinf=0.0, neginf=0.0)).long()
+    b = torch.where(x < LO, 0, torch.where(~(x < HI), NB + 1, inner))[sel]
+    assert torch.equal(torch.bincount(b, minlength=NB + 2), h)
+    del x, qq, inner, b
+    ev = _sample_idx(n, seed=9)
+    ev = ev[host(sel[torch.from_numpy(ev).cuda()])]
+    assert ev.size > 300
+    for e0 in ev[:400]:
+        hm, hq, ho = synth.jagged_events(int(e0), 1, dtype=np.float64)
+        _, mo, s = O.dimuon_histogram(hm, hq, ho, LO, HI, NB)
+        assert s == 1
+        _, e = O.invariant_mass(hm[:1], hm[1:2])
+        assert mass_violations(host(m_out[int(e0):int(e0) + 1]), mo, e, 1e-12).size == 0
