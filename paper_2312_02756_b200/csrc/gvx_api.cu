@@ -238,37 +238,38 @@ template <typename T, int C, int MODE>
 gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, void* m_out,
                            const HistParams& hp, unsigned long long* bins, const gvx_vec4_view* bo, cudaStream_t s,
                            const CosOut<T>& co = CosOut<T>{}) {
-  if constexpr (MODE == PM_HIST_CM_COS)
-    return launch_pair_tma_cfg<T, C, MODE, typename TmaCfgOf<T, MODE>::type>(v1, v2, n, m_out, hp, bins, bo, s, co);
 #ifdef GVX_TUNE
   if constexpr (sizeof(T) == 8 && C == C_PTETAPHIM) {
     switch (tune_env("GVX_TMA_CFG")) {
-      case 1: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 4, 8, 3>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 2: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 512, 2, 8, 3>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 3: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 3, 8, 4>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 4: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 512, 6, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 5: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 6, 8, 2>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 6: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 768, 4, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 7: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 640, 5, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 8: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 896, 3, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 9: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 992, 3, 31, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 10: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 448, 3, 14, 2>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 11: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 896, 2, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 12: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1024, 3, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 13: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1280, 2, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 1: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 4, 8, 3>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 2: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 512, 2, 8, 3>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 3: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 3, 8, 4>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 4: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 512, 6, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 5: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 256, 6, 8, 2>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 6: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 768, 4, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 7: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 640, 5, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 8: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 896, 3, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 9: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 992, 3, 31, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 10: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 448, 3, 14, 2>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 11: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 896, 2, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 12: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1024, 3, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 13: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1280, 2, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       default: break;
     }
   }
   if constexpr (sizeof(T) == 4 && C == C_PTETAPHIM) {
     switch (tune_env("GVX_TMA_CFG32")) {
-      case 1: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1792, 3, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 2: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 896, 4, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
-      case 3: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1024, 3, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s);
+      case 1: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1792, 3, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 2: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 896, 4, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 3: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1024, 3, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 4: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 768, 4, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 5: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 512, 4, 16, 2>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 6: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1536, 4, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       default: break;
     }
   }
 #endif
-  return launch_pair_tma_cfg<T, C, MODE, typename TmaCfgOf<T, MODE>::type>(v1, v2, n, m_out, hp, bins, bo, s);
+  return launch_pair_tma_cfg<T, C, MODE, typename TmaCfgOf<T, MODE>::type>(v1, v2, n, m_out, hp, bins, bo, s, co);
 }
 
 // ---------------------------------------------------------------- mass ------

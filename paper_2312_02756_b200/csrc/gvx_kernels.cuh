@@ -785,6 +785,42 @@ __device__ __forceinline__ void pair_consume(const T (&a)[4], const T (&b)[4], i
   }
 }
 
+// fp32 CM modes, two events of a thread at once in packed FFMA2/FMUL2/FADD2
+// arithmetic (cm_mass_f32_lanes<float2>: the same bits as the scalar path);
+// a pair with an event outside the fast domain takes the scalar path.
+template <int COORDS, int MODE>
+__device__ __forceinline__ void pair_consume_x2(const float (&a0)[4], const float (&b0)[4], const float (&a1)[4],
+                                                const float (&b1)[4], int64_t i0, int64_t i1, float* __restrict__ m_out,
+                                                unsigned int* sh_hist, const HistParams& hp, const View4o<float>& bo,
+                                                unsigned int* sh_cos, const CosOut<float>& co) {
+  if (fast_domain(a0[0], a0[1], a0[2], a0[3]) & fast_domain(b0[0], b0[1], b0[2], b0[3]) &
+      fast_domain(a1[0], a1[1], a1[2], a1[3]) & fast_domain(b1[0], b1[1], b1[2], b1[3])) {
+    constexpr bool COS = MODE == PM_HIST_CM_COS;
+    float2 c;
+    const float2 M = cm_mass_f32_lanes<float2, COS, false>(
+        make_float2(a0[0], a1[0]), make_float2(a0[1], a1[1]), make_float2(a0[2], a1[2]), make_float2(a0[3], a1[3]),
+        make_float2(b0[0], b1[0]), make_float2(b0[1], b1[1]), make_float2(b0[2], b1[2]), make_float2(b0[3], b1[3]),
+        &c, nullptr);
+    atomicAdd(&sh_hist[find_bin((double)M.x, hp)], 1u);
+    atomicAdd(&sh_hist[find_bin((double)M.y, hp)], 1u);
+    if (m_out) {
+      m_out[i0] = M.x;
+      m_out[i1] = M.y;
+    }
+    if constexpr (COS) {
+      atomicAdd(&sh_cos[find_bin((double)c.x, co.hc)], 1u);
+      atomicAdd(&sh_cos[find_bin((double)c.y, co.hc)], 1u);
+      if (co.cos_out) {
+        co.cos_out[i0] = c.x;
+        co.cos_out[i1] = c.y;
+      }
+    }
+  } else {
+    pair_consume<float, COORDS, MODE, false>(a0, b0, i0, m_out, sh_hist, hp, bo, sh_cos, co);
+    pair_consume<float, COORDS, MODE, false>(a1, b1, i1, m_out, sh_hist, hp, bo, sh_cos, co);
+  }
+}
+
 // SOA = false: each stage holds the v1 and v2 AoS tiles (2 bulk copies);
 // SOA = true: the 8 component tiles of v1 and v2 (8 bulk copies), read back
 // lane-contiguously (LDS.64 / LDS.32, no bank conflicts).
@@ -880,10 +916,20 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
 #endif
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
+      constexpr bool PACK = sizeof(T) == 4 && (MODE == PM_HIST_CM || MODE == PM_HIST_CM_COS) &&
+                            COORDS == C_PTETAPHIM && !WANT_BO && CFG::EPT % 2 == 0;
+      if constexpr (PACK) {
 #pragma unroll
-      for (int u = 0; u < CFG::EPT; ++u)
-        pair_consume<T, COORDS, MODE, WANT_BO>(a[u], b[u], t * CFG::TILE + u * CFG::NCT + ctid, m_out, sh_hist, hp,
-                                               bo, sh_cos, co);
+        for (int u = 0; u < CFG::EPT; u += 2)
+          pair_consume_x2<COORDS, MODE>(a[u], b[u], a[u + 1], b[u + 1], t * CFG::TILE + u * CFG::NCT + ctid,
+                                        t * CFG::TILE + (u + 1) * CFG::NCT + ctid, m_out, sh_hist, hp, bo, sh_cos,
+                                        co);
+      } else {
+#pragma unroll
+        for (int u = 0; u < CFG::EPT; ++u)
+          pair_consume<T, COORDS, MODE, WANT_BO>(a[u], b[u], t * CFG::TILE + u * CFG::NCT + ctid, m_out, sh_hist,
+                                                 hp, bo, sh_cos, co);
+      }
       if (++s == CFG::STAGES) { s = 0; ph ^= 1u; }
     }
     // ragged tail (< TILE events): the last CTA, plain loads

@@ -514,9 +514,36 @@ __device__ __forceinline__ float pos_sqrt(float x) { return fast_sqrt(x > 0.f ? 
 // to both vectors literally, but vector 1 becomes (pt1, 0, pt1 sinh eta1, E1)
 // and vector 2 needs only sin/cos of phi2 - phi1 — one sincos per pair instead
 // of two. Boosted vectors, when requested, are rotated back by +phi1.
+template <typename V, bool WANT_COS, bool WANT_VEC>
+__device__ __forceinline__ V cm_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt2, V eta2, V phi2, V m2,
+                                               V* cos_out, V* vec_out);
+
 template <typename T, bool WANT_COS = false>
 __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1, T pt2, T eta2, T phi2, T m2,
                                                     V4<T>* a_out, V4<T>* b_out, T* cos_out = nullptr) {
+  if constexpr (sizeof(T) == 4) {  // fp32: the lane core (bit-identical to its packed two-event form)
+    T M;
+    if (a_out) {
+      T v[8];
+      M = cm_mass_f32_lanes<float, WANT_COS, true>(pt1, eta1, phi1, m1, pt2, eta2, phi2, m2, cos_out, v);
+      *a_out = V4<T>{v[0], v[1], v[2], v[3]};
+      *b_out = V4<T>{v[4], v[5], v[6], v[7]};
+    } else {
+      M = cm_mass_f32_lanes<float, WANT_COS, false>(pt1, eta1, phi1, m1, pt2, eta2, phi2, m2, cos_out, nullptr);
+    }
+    if (a_out) {
+      T s1, c1;
+      fast_sincos(phi1, s1, c1);
+      V4<T>* v[2] = {a_out, b_out};
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        T x = v[i]->x, y = v[i]->y;
+        v[i]->x = c1 * x - s1 * y;
+        v[i]->y = s1 * x + c1 * y;
+      }
+    }
+    return M;
+  }
   T sd, cd, sh1, ch1, sh2, ch2;
   fast_sincos(phi2 - phi1, sd, cd);
   sinh_cosh(eta1, sh1, ch1);
@@ -537,6 +564,118 @@ __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1,
     }
   }
   return M;
+}
+
+// ---------------------------------------------------------------------------
+// fp32 CM mass written once over a "lane vector" V = float (one event) or
+// float2 (two events in the packed FFMA2 / FMUL2 / FADD2 instructions of
+// sm_100: half the FP32 issue slots of the issue-bound f32 CM kernels). Every
+// FP32 operation is explicit (no compiler contraction), so the scalar and the
+// packed instantiation produce the same bits for the same event; MUFU
+// operations (ex2, rcp, rsqrt, sqrt, sin/cos) and compares act per lane.
+// Same formulas and rotated frame as cm_mass_ptetaphim_fast (fast domain).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float lv_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float lv_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float lv_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ float lv_splat(float, float x) { return x; }
+// Packed ops as PTX. Note: ptxas still contracts a packed mul feeding a packed
+// add into FFMA2 (measured: g*x + g*y became one FFMA2, 1 ulp off the scalar
+// path for ~20 % of events), so cm_mass_f32_lanes writes every such sum as an
+// explicit fma.
+__device__ __forceinline__ float2 lv_mul(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 x, y, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
+      "mul.rn.f32x2 z, x, y;\n\tmov.b64 {%0, %1}, z;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 lv_add(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 x, y, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
+      "add.rn.f32x2 z, x, y;\n\tmov.b64 {%0, %1}, z;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 lv_fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 x, y, w, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\tmov.b64 w, {%6, %7};\n\t"
+      "fma.rn.f32x2 z, x, y, w;\n\tmov.b64 {%0, %1}, z;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 lv_splat(float2, float x) { return make_float2(x, x); }
+template <typename F> __device__ __forceinline__ float lv_map(float a, F f) { return f(a); }
+template <typename F> __device__ __forceinline__ float2 lv_map(float2 a, F f) { return make_float2(f(a.x), f(a.y)); }
+template <typename F> __device__ __forceinline__ float lv_map2(float a, float b, F f) { return f(a, b); }
+template <typename F> __device__ __forceinline__ float2 lv_map2(float2 a, float2 b, F f) {
+  return make_float2(f(a.x, b.x), f(a.y, b.y));
+}
+
+// vec_out (WANT_VEC): the boosted pair in the rotated frame, (a2x, a2y, a2z, a2t, b2x, b2y, b2z, b2t).
+template <typename V, bool WANT_COS, bool WANT_VEC>
+__device__ __forceinline__ V cm_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt2, V eta2, V phi2, V m2,
+                                               V* cos_out, V* vec_out) {
+  const V ONE = lv_splat(V{}, 1.f), MONE = lv_splat(V{}, -1.f), HALF = lv_splat(V{}, 0.5f);
+  const V LOG2E = lv_splat(V{}, 1.44269504088896341f);
+  // sin/cos of phi2 - phi1 after one Cody-Waite step to [-pi, pi] (as reduce_2pi)
+  V d = lv_fma(phi1, MONE, phi2);
+  V k = lv_map(lv_mul(d, lv_splat(V{}, 0.159154943091895336f)), [](float x) { return rintf(x); });
+  V r = lv_fma(k, lv_splat(V{}, -6.28318548202514648f), d);
+  r = lv_fma(k, lv_splat(V{}, 1.74845553146951715e-7f), r);
+  V sd = lv_map(r, [](float x) { return __sinf(x); }), cd = lv_map(r, [](float x) { return __cosf(x); });
+  // sinh/cosh from one ex2 and its reciprocal
+  V e1 = lv_map(lv_mul(eta1, LOG2E), [](float x) { return fast_ex2(x); });
+  V e2 = lv_map(lv_mul(eta2, LOG2E), [](float x) { return fast_ex2(x); });
+  V r1 = lv_map(e1, [](float x) { return fast_rcp(x); }), r2 = lv_map(e2, [](float x) { return fast_rcp(x); });
+  V sh1 = lv_mul(lv_fma(r1, MONE, e1), HALF), ch1 = lv_mul(lv_add(e1, r1), HALF);
+  V sh2 = lv_mul(lv_fma(r2, MONE, e2), HALF), ch2 = lv_mul(lv_add(e2, r2), HALF);
+  V q1 = lv_mul(pt1, ch1), q2 = lv_mul(pt2, ch2);
+  auto pos_sqrt_f = [](float x) { return fast_sqrt(x > 0.f ? x : 0.f); };
+  // vector 1 in the rotated frame: (pt1, 0, pt1 sh1, E1); vector 2: (pt2 cd, pt2 sd, pt2 sh2, E2)
+  V ax = pt1, az = lv_mul(pt1, sh1);
+  V aE = lv_map(lv_fma(m1, lv_map(m1, [](float x) { return fabsf(x); }), lv_mul(q1, q1)), pos_sqrt_f);
+  V bx = lv_mul(pt2, cd), by = lv_mul(pt2, sd), bz = lv_mul(pt2, sh2);
+  V bE = lv_map(lv_fma(m2, lv_map(m2, [](float x) { return fabsf(x); }), lv_mul(q2, q2)), pos_sqrt_f);
+  // beta_cm = -P / E (P_y = b_y: vector 1 has no y component in this frame)
+  // every sum whose operand is a product is an explicit fma: ptxas contracts
+  // mul.rn.f32x2 + add.rn.f32x2 pairs (unlike the scalar .rn forms), which
+  // would make the packed path differ from the scalar one by an ulp
+  V Px = lv_fma(pt2, cd, ax), Pz = lv_fma(pt2, sh2, az), E = lv_add(aE, bE);
+  V ninv = lv_map(E, [](float x) { return -fast_rcp(x); });
+  V betx = lv_mul(Px, ninv), bety = lv_mul(by, ninv), betz = lv_mul(Pz, ninv);
+  V u = lv_fma(lv_fma(betz, betz, lv_fma(bety, bety, lv_mul(betx, betx))), MONE, ONE);  // 1 - beta^2
+  // gamma = u^-1/2, gamma^2/(1+gamma) = 1/(u + u gamma); invalid (E <= 0, beta^2 >= 1, NaN) -> NaN
+  V g = lv_map2(u, E, [](float uu, float ee) {
+    float gg;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(gg) : "f"(uu));
+    return (uu > 0.f && ee > 0.f) ? gg : __int_as_float(0x7fffffff);
+  });
+  V bg = lv_map(lv_fma(u, g, u), [](float x) { return fast_rcp(x); });
+  // boost vector 1 (y = 0) and vector 2, literally (SPEC.md:188 with R6)
+  V bpa = lv_fma(betz, az, lv_mul(betx, ax));
+  V fa = lv_fma(bg, bpa, lv_mul(g, aE));
+  V a2x = lv_fma(fa, betx, ax), a2y = lv_mul(fa, bety), a2z = lv_fma(fa, betz, az), a2t = lv_mul(g, lv_add(aE, bpa));
+  V bpb = lv_fma(betz, bz, lv_fma(bety, by, lv_mul(betx, bx)));
+  V fb = lv_fma(bg, bpb, lv_mul(g, bE));
+  V b2x = lv_fma(fb, betx, bx), b2y = lv_fma(fb, bety, by), b2z = lv_fma(fb, betz, bz), b2t = lv_mul(g, lv_add(bE, bpb));
+  if constexpr (WANT_VEC) {
+    vec_out[0] = a2x; vec_out[1] = a2y; vec_out[2] = a2z; vec_out[3] = a2t;
+    vec_out[4] = b2x; vec_out[5] = b2y; vec_out[6] = b2z; vec_out[7] = b2t;
+  }
+  V X = lv_add(a2x, b2x), Y = lv_fma(fa, bety, b2y), Z = lv_add(a2z, b2z);
+  V W = lv_fma(g, lv_add(aE, bpa), b2t);
+  V p2 = lv_fma(Z, Z, lv_fma(Y, Y, lv_mul(X, X)));
+  V m2sq = lv_fma(W, W, lv_mul(p2, MONE));
+  if constexpr (WANT_COS) {
+    V pa = lv_fma(a2z, a2z, lv_fma(a2y, a2y, lv_mul(a2x, a2x)));
+    *cos_out = lv_mul(a2z, lv_map(pa, [](float x) {
+                        float y;
+                        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+                        return y;
+                      }));
+  }
+  return lv_map(m2sq, [](float x) { return x >= 0.f ? fast_sqrt(x) : -fast_sqrt(-x); });
 }
 
 // ---------------------------------------------------------------------------
