@@ -97,12 +97,60 @@ def oracle_step_rate(n_sample: int, dtype: str, repeats: int = 3):
     return n_sample / best, best
 
 
+def oracle_step_rate_all_cores(n_sample: int, dtype: str, repeats: int = 3):
+    """The same oracle step over static contiguous chunks, one host thread per core this
+    process may run on ("all cores"; ctypes releases the GIL in the C calls)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    import oracle
+    import synth
+    cores = len(os.sched_getaffinity(0))
+    dt = np.float64 if dtype == "f64" else np.float32
+    idx = np.arange(n_sample)
+    v1, v2 = synth.muon_pairs(idx, dtype=dt)
+    v, b = synth.boost_inputs(idx, dtype=dt)
+    bounds = [(n_sample * c // cores, n_sample * (c + 1) // cores) for c in range(cores)]
+
+    def chunk(ab):
+        a, z = ab
+        oracle.invariant_mass(v1[a:z], v2[a:z])
+        oracle.boost(v[a:z], b[a:z])
+        oracle.mass_histogram(v1[a:z], v2[a:z], LO, HI, NB)
+        oracle.mass_histogram(v1[a:z], v2[a:z], LO, HI, NB, cm=True)
+
+    best = float("inf")
+    with ThreadPoolExecutor(cores) as ex:
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            list(ex.map(chunk, bounds))
+            best = min(best, time.perf_counter() - t0)
+    return n_sample / best, best, cores
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_obj(n_sample: int, dtype: str):
     rate, t = oracle_step_rate(n_sample, dtype)
+    rate_all, t_all, cores = oracle_step_rate_all_cores(n_sample, dtype)
     return {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{n_sample} events of the same synthetic workload ({dtype}), one full step "
                       f"(mass + boost + lab histogram + CM histogram), single-threaded C oracle "
-                      f"(gcc -O2 -ffp-contract=off), best of 3 ({t:.2f} s)"}
+                      f"(gcc -O2 -ffp-contract=off), best of 3 ({t:.2f} s)",
+            "cpu": cpu_model(),
+            "all_cores": {"value": rate_all, "unit": UNIT, "cores": cores,
+                          "sample": f"the same {n_sample} events in {cores} static contiguous chunks, one "
+                                    f"host thread per core, best of 3 ({t_all:.2f} s)"}}
 
 
 def run_reference(args):
