@@ -80,6 +80,31 @@ def test_validation_codes(gvx):
     assert H(gvx.GVX_F64, 0, by(a), by(b), 0, 0.0, 1.0, 10, None, 0, None, None, None) == 0
 
 
+def test_cm_costheta_validation(gvx):
+    """gvx_cm_costheta_histogram (ABI v3) validates both axes, both bin arrays and the
+    optional outputs synchronously; n == 0 is OK with nothing launched."""
+    L = gvx.lib
+    by = ctypes.byref
+    a, b = _view(), _view()
+    C = L.gvx_cm_costheta_histogram
+    ok_m, ok_c = (0.25, 300.0, 1000), (-1.0, 1.0, 100)
+
+    def call(n=4, m=ok_m, c=ok_c, mb=0x4000, cb=0x5000, mo=None, co=None, dt=gvx.GVX_F64, coords=0):
+        return C(dt, coords, by(a), by(b), n, m[0], m[1], m[2], mb, c[0], c[1], c[2], cb, mo, co, None)
+
+    assert call(m=(1.0, 1.0, 10)) == 1                    # lo >= hi (mass axis)
+    assert call(c=(1.0, -1.0, 10)) == 1                   # lo >= hi (angle axis)
+    assert call(c=(-1.0, float("nan"), 10)) == 1          # non-finite edge
+    assert call(m=(0.0, 1.0, 0)) == 1                     # nbins < 1
+    assert call(c=(0.0, 1.0, 1 << 29)) == 1               # nbins too large
+    assert call(mb=None) == 1 and call(cb=None) == 1      # missing bins
+    assert call(cb=0x5004) == 1                           # misaligned bins
+    assert call(co=0x6001) == 1                           # misaligned cos output
+    assert call(dt=7) == 1 and call(coords=9) == 1 and call(n=-1) == 1
+    assert call(n=0, mb=None, cb=None) == 0               # n == 0: OK, nothing launched (SPEC.md:280)
+    assert call(n=0, m=(1.0, 1.0, 10)) == 1               # ... but a bad axis is still an error
+
+
 def test_lorentz_matrix_validation(gvx):
     """gvx_lorentz_transform checks L^T g L = g on the host before anything is enqueued."""
     L = gvx.lib
