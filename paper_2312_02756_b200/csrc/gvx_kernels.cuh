@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
     __syncthreads();
   }
   auto count = [&](T M) {
-    int b = find_bin((double)M, hp);
+    int b = find_bin(M, hp);
     if constexpr (SMEM) atomicAdd(&sh[b], 1u);
     else atomicAdd(&bins[b], 1ull);
   };
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(256) k_cm_costheta(View4<T> v1, View4<T> v2, i
     load_event(v1, i, x);
     load_event(v2, i, y);
     T M = hist_event_mass<T, COORDS, true, false, true>(x, y, i, none, &c);
-    const int bm = find_bin((double)M, hm), bc = find_bin((double)c, hc);
+    const int bm = find_bin(M, hm), bc = find_bin(c, hc);
     if constexpr (SMEM) {
       atomicAdd(&shc[bm], 1u);
       atomicAdd(&shc[nm + bc], 1u);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(256) k_dimuon_histogram(View4<T> mu, const int
       T M = T(NAN);
       if (sel[u]) {
         M = event_mass<T, C_PTETAPHIM>(a[u], b[u]);
-        atomicAdd(&shd[find_bin((double)M, hp)], 1u);
+        atomicAdd(&shd[find_bin(M, hp)], 1u);
       }
       if (m_out) m_out[e] = M;
     }
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_compact(View4<T> mu, const 
       for (int u = 0; u < U; ++u) {
         if (el[u] < 0) break;
         const T M = event_mass<T, C_PTETAPHIM>(a[u], b[u]);
-        atomicAdd(&s_hist[find_bin((double)M, hp)], 1u);
+        atomicAdd(&s_hist[find_bin(M, hp)], 1u);
         if (m_out) m_out[e0 + el[u]] = M;
       }
     }
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
         T M = T(NAN);
         if (sel[u]) {
           M = event_mass<T, C_PTETAPHIM>(a[u], b[u]);
-          atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+          atomicAdd(&sh_hist[find_bin(M, hp)], 1u);
         }
         if (m_out) m_out[t * CFG::ET + u * CFG::NCT + ctid] = M;
       }
@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
 #pragma unroll
           for (int c = 0; c < 4; ++c) { a[c] = mu[4 * o + c]; b[c] = mu[4 * o + 4 + c]; }
           M = event_mass<T, C_PTETAPHIM>(a, b);
-          atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+          atomicAdd(&sh_hist[find_bin(M, hp)], 1u);
         }
         if (m_out) m_out[e] = M;
       }
@@ -774,13 +774,13 @@ __device__ __forceinline__ void pair_consume(const T (&a)[4], const T (&b)[4], i
   } else if constexpr (MODE == PM_HIST_CM_COS) {
     T c;
     T M = hist_event_mass<T, COORDS, true, WANT_BO, true>(a, b, i, bo, &c);
-    atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
-    atomicAdd(&sh_cos[find_bin((double)c, co.hc)], 1u);
+    atomicAdd(&sh_hist[find_bin(M, hp)], 1u);
+    atomicAdd(&sh_cos[find_bin(c, co.hc)], 1u);
     if (m_out) m_out[i] = M;
     if (co.cos_out) co.cos_out[i] = c;
   } else {
     T M = hist_event_mass<T, COORDS, MODE == PM_HIST_CM, WANT_BO>(a, b, i, bo);
-    atomicAdd(&sh_hist[find_bin((double)M, hp)], 1u);
+    atomicAdd(&sh_hist[find_bin(M, hp)], 1u);
     if (m_out) m_out[i] = M;
   }
 }
@@ -801,15 +801,15 @@ __device__ __forceinline__ void pair_consume_x2(const float (&a0)[4], const floa
         make_float2(a0[0], a1[0]), make_float2(a0[1], a1[1]), make_float2(a0[2], a1[2]), make_float2(a0[3], a1[3]),
         make_float2(b0[0], b1[0]), make_float2(b0[1], b1[1]), make_float2(b0[2], b1[2]), make_float2(b0[3], b1[3]),
         &c, nullptr);
-    atomicAdd(&sh_hist[find_bin((double)M.x, hp)], 1u);
-    atomicAdd(&sh_hist[find_bin((double)M.y, hp)], 1u);
+    atomicAdd(&sh_hist[find_bin(M.x, hp)], 1u);
+    atomicAdd(&sh_hist[find_bin(M.y, hp)], 1u);
     if (m_out) {
       m_out[i0] = M.x;
       m_out[i1] = M.y;
     }
     if constexpr (COS) {
-      atomicAdd(&sh_cos[find_bin((double)c.x, co.hc)], 1u);
-      atomicAdd(&sh_cos[find_bin((double)c.y, co.hc)], 1u);
+      atomicAdd(&sh_cos[find_bin(c.x, co.hc)], 1u);
+      atomicAdd(&sh_cos[find_bin(c.y, co.hc)], 1u);
       if (co.cos_out) {
         co.cos_out[i0] = c.x;
         co.cos_out[i1] = c.y;

@@ -751,6 +751,9 @@ struct HistParams {
   double scale;          // nbins_d / width
   int nbins;
   uint32_t near_hi;      // high word of 1e-14 * nbins: |d| with abs_hi(d) <= near_hi is "near"
+  // fp32 masses (find_bin(float)): the same scheme in FP32 with a wider near-edge window
+  float lo_f, scale_f, near_f;
+  int f32_ok;            // nbins <= 2^20 and the float parameters are finite
 };
 
 inline HistParams make_hist_params(double lo, double hi, int nbins) {
@@ -765,6 +768,14 @@ inline HistParams make_hist_params(double lo, double hi, int nbins) {
   uint64_t bits;
   memcpy(&bits, &tol, 8);
   hp.near_hi = (uint32_t)(bits >> 32);
+  // fp32 path: q_f = RN(RN(x - lo_f) * scale_f) is within 3 float ulps of q (relative 1.8e-7)
+  // plus |lo_f - lo| * scale; the window is 4x that bound on the in-range |q| <= nbins.
+  hp.lo_f = (float)lo;
+  hp.scale_f = (float)hp.scale;
+  const double lo_err = fabs((double)hp.lo_f - lo) * hp.scale;
+  hp.near_f = (float)(4.0 * (1.8e-7 * (hp.nbins_d + 1.0) + lo_err) + 1e-30);
+  hp.f32_ok = nbins <= (1 << 20) && isfinite(hp.lo_f) && isfinite(hp.scale_f) && hp.scale_f > 0.f &&
+              hp.near_f < 0.25f;
   return hp;
 }
 
@@ -772,6 +783,26 @@ __device__ __noinline__ int find_bin_exact(double x, const HistParams& hp) {
   if (x < hp.lo) return 0;
   if (!(x < hp.hi)) return hp.nbins + 1;
   return 1 + __double2int_rz(__ddiv_rn(__dmul_rn(hp.nbins_d, __dsub_rn(x, hp.lo)), hp.width));
+}
+
+__device__ __forceinline__ int find_bin(double x, const HistParams& hp);
+
+// fp32 value: the oracle promotes it to double and bins there (R12); the same
+// shifter scheme in FP32 (t = q + 1.5*2^23, k = rint(q) from t's bits, |q| < 2^22)
+// decides every event whose q is more than near_f from an integer, the rest (and
+// non-finite x) take the double path. Saves the F2F.F64 (XU) and the DP ops in the
+// issue-bound fp32 kernels.
+__device__ __forceinline__ int find_bin(float x, const HistParams& hp) {
+  if (!hp.f32_ok) return find_bin((double)x, hp);
+  const float MAGIC = 12582912.f;  // 1.5 * 2^23
+  const float q = __fmul_rn(__fsub_rn(x, hp.lo_f), hp.scale_f);
+  const float t = __fadd_rn(q, MAGIC);
+  const int k = __float_as_int(t) - 0x4B400000;
+  const float d = __fsub_rn(q, __fsub_rn(t, MAGIC));
+  const bool in = (unsigned)k <= (unsigned)hp.nbins;
+  int bin = in ? 1 + k - (__float_as_int(d) < 0 ? 1 : 0) : (__float_as_int(q) < 0 ? 0 : hp.nbins + 1);
+  if ((in & (fabsf(d) <= hp.near_f)) | ((__float_as_int(x) & 0x7fffffff) >= 0x7f800000)) bin = find_bin_exact((double)x, hp);
+  return bin;
 }
 
 __device__ __forceinline__ int find_bin(double x, const HistParams& hp) {
