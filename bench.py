@@ -55,6 +55,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=1 << 22, help="events in the oracle's bounded sample")
     p.add_argument("--dist-backend", default="nccl", help="process-group backend for N>1 (nccl on B200s)")
+    p.add_argument("--bin-reduce", choices=["nccl", "p2p"], default="nccl",
+                   help="N>1 bin reduction: NCCL all-reduce after the kernel, or fused into the kernel tail "
+                        "(P2P atomics into every rank's symmetric-memory bins, SURVEY 8(e))")
     p.add_argument("--sweep", action="store_true", help="N sweep (CFG2 shape) instead of the step benchmark")
     p.add_argument("--extended", action="store_true",
                    help="also time the widened rows (other coordinate systems, SoA, uniform boost) at N")
@@ -203,7 +206,10 @@ def config_obj(args, world, ref_sample=None):
          "n_events_per_gpu": n, "global_events": n * world, "layout": "AoS",
          "hist": {"lo": LO, "hi": HI, "nbins": NB},
          "l2": f"inputs larger than L2 ({in_bytes / 1e9:.1f} GB per GPU >> 126 MB), no flush needed",
-         "parallelism": f"dp{world} (event-index shards, {getattr(args, 'dist_backend', 'nccl')} bin all-reduce)"}
+         "parallelism": f"dp{world} (event-index shards, " + (
+             "bin all-reduce fused into the kernel tail: P2P atomics into symmetric memory)"
+             if world > 1 and getattr(args, "bin_reduce", "nccl") == "p2p" and getattr(args, "dist_backend", "nccl") == "nccl"
+             else f"{getattr(args, 'dist_backend', 'nccl')} bin all-reduce)")}
     if ref_sample:
         c["reference_sample_events"] = ref_sample
     return c
@@ -309,6 +315,7 @@ def run_ours(args):
     bins_cm = gvx.new_bins(NB, dev)
     torch.cuda.synchronize(dev)
 
+    p2p = world > 1 and args.bin_reduce == "p2p" and args.dist_backend == "nccl"
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     kern_ms = {k: [] for k in KERNEL_ORDER}
 
@@ -323,6 +330,14 @@ def run_ours(args):
         gvx.boost(bv, bb, out=bout)
         if record:
             ev[2].record(stream)
+        if p2p:  # reduction fused into the histogram kernels (barriers included in their time)
+            gvx.allreduce_mass_histogram(v1, v2, LO, HI, NB, slot=0)
+            if record:
+                ev[3].record(stream)
+            gvx.allreduce_mass_histogram(v1, v2, LO, HI, NB, cm=True, slot=1)
+            if record:
+                ev[4].record(stream)
+            return
         gvx.mass_histogram(v1, v2, LO, HI, NB, bins=bins)
         if record:
             ev[3].record(stream)

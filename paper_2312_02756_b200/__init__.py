@@ -43,7 +43,7 @@ GVX_PXPYPZE = 1
 GVX_PXPYPZM = 2
 GVX_PTETAPHIE = 3
 GVX_HIST_BOOST_TO_CM = 0x1
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # The default histogram of the north star: 1000 bins over the dimuon range
 # (reading R13).
@@ -100,6 +100,10 @@ def _load_lib():
     lib.gvx_dimuon_histogram.argtypes = [st, ctypes.POINTER(Vec4CView), P, P, I64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_int32, P, P, P]
     lib.gvx_dimuon_histogram.restype = st
+    lib.gvx_mass_histogram_peers.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
+                                             ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, ctypes.c_int32,
+                                             P, ctypes.c_uint32, P, P]
+    lib.gvx_mass_histogram_peers.restype = st
     lib.gvx_cm_costheta_histogram.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
                                               ctypes.c_double, ctypes.c_double, ctypes.c_int32, P,
                                               ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P, P]
@@ -404,6 +408,68 @@ def sharded_mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: f
     Returns the global histogram on every rank."""
     bins = mass_histogram(v1, v2, lo, hi, nbins, bins=bins, cm=cm, coords=coords)
     return allreduce_bins(bins, group)
+
+
+def mass_histogram_peers(v1: VecArg, v2: VecArg, peer_bins_dev: int, npeers: int, lo: float = DEFAULT_LO,
+                         hi: float = DEFAULT_HI, nbins: int = DEFAULT_NBINS, cm: bool = False,
+                         m_out: Optional[torch.Tensor] = None, coords: str = "ptetaphim",
+                         mc_bins: Optional[int] = None) -> None:
+    """gvx_mass_histogram_peers: the fused histogram whose CTAs add their counts straight into
+    every peer's bins (``peer_bins_dev``: device address of an array of ``npeers`` device
+    pointers) or into one multicast address (``mc_bins``). The caller owns the cross-rank
+    barriers around the call (see allreduce_mass_histogram)."""
+    a, n, dt, dev, _ = _view(v1, 4, "v1")
+    b, n2, dt2, dev2, _ = _view(v2, 4, "v2")
+    if n != n2:
+        raise ValueError(f"length mismatch: v1 has {n} vectors, v2 has {n2}")
+    if dt != dt2 or dev != dev2:
+        raise ValueError("v1 and v2 must share dtype and device")
+    mptr = _out_1d(m_out, n, dt, "m_out")
+    with torch.cuda.device(dev):
+        _check(lib.gvx_mass_histogram_peers(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b), n,
+                                            float(lo), float(hi), int(nbins), int(peer_bins_dev) or None,
+                                            int(npeers), mc_bins, GVX_HIST_BOOST_TO_CM if cm else 0, mptr,
+                                            _stream(dev)), "gvx_mass_histogram_peers")
+
+
+_SYMM_BINS = {}
+
+
+def allreduce_mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = DEFAULT_HI,
+                             nbins: int = DEFAULT_NBINS, cm: bool = False, group=None,
+                             coords: str = "ptetaphim", multicast: bool = False, slot: int = 0) -> torch.Tensor:
+    """Global histogram of every rank's shard with the all-reduce fused into the kernel tail
+    (SURVEY §8(e)): the bins live in torch symmetric memory (one int64[nbins+2] per rank,
+    peer-mapped over NVLink); a device barrier after zeroing, the kernel adds each CTA's counts
+    into all ranks' bins (P2P atomics, or one multimem.red to the NVSwitch multicast address when
+    ``multicast`` and the group supports it), a device barrier, and every rank holds the total.
+    Returns this rank's symmetric bins tensor, one per (group, nbins, device, ``slot``), reused
+    across calls: copy it (or use another slot) to keep a result."""
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    a, _, _, dev, _ = _view(v1, 4, "v1")
+    group = group or dist.group.WORLD
+    key = (id(group), nbins, dev.index, slot)
+    if key not in _SYMM_BINS:
+        bins = symm.empty(nbins + 2, dtype=torch.int64, device=dev)
+        hdl = symm.rendezvous(bins, group)
+        # this tensor's address in every rank's mapping (its offset inside the symmetric buffer
+        # is the same on all ranks), as a device array for the kernel
+        off = bins.data_ptr() - int(hdl.buffer_ptrs[hdl.rank])
+        ptrs = torch.tensor([int(p) + off for p in hdl.buffer_ptrs], dtype=torch.int64, device=dev)
+        try:  # 0 when the group has no NVSwitch multicast object
+            mcp = int(hdl.multicast_ptr or 0)
+        except (RuntimeError, TypeError):
+            mcp = 0
+        mc = mcp + off if mcp else None
+        _SYMM_BINS[key] = (bins, hdl, ptrs, mc)
+    bins, hdl, ptrs, mc = _SYMM_BINS[key]
+    bins.zero_()
+    hdl.barrier(channel=0)
+    mass_histogram_peers(v1, v2, ptrs.data_ptr(), ptrs.numel(), lo, hi, nbins, cm=cm, coords=coords,
+                         mc_bins=mc if multicast else None)
+    hdl.barrier(channel=0)
+    return bins
 
 
 def allreduce_bins(bins: torch.Tensor, group=None) -> torch.Tensor:

@@ -732,9 +732,35 @@ gvx_status gvx_cm_costheta_histogram(gvx_dtype dtype, gvx_coords coords, const g
 #undef GVX_COS_COORDS
 }
 
+static gvx_status mass_histogram_impl(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,
+                                      const gvx_vec4_cview* v2, int64_t n, double lo, double hi, int32_t nbins,
+                                      unsigned long long* bins, uint32_t flags, void* m_out,
+                                      const gvx_vec4_view* boosted_out, gvx_stream_t stream,
+                                      unsigned long long* const* peers, int32_t npeers, unsigned long long* mc);
+
 gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1, const gvx_vec4_cview* v2,
                               int64_t n, double lo, double hi, int32_t nbins, unsigned long long* bins, uint32_t flags,
                               void* m_out, const gvx_vec4_view* boosted_out, gvx_stream_t stream) {
+  return mass_histogram_impl(dtype, coords, v1, v2, n, lo, hi, nbins, bins, flags, m_out, boosted_out, stream,
+                             nullptr, 0, nullptr);
+}
+
+gvx_status gvx_mass_histogram_peers(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,
+                                    const gvx_vec4_cview* v2, int64_t n, double lo, double hi, int32_t nbins,
+                                    unsigned long long* const* peer_bins, int32_t npeers,
+                                    unsigned long long* mc_bins, uint32_t flags, void* m_out, gvx_stream_t stream) {
+  if (mc_bins ? !aligned(mc_bins, 8) : (!peer_bins || !aligned(peer_bins, 8) || npeers < 1 || npeers > 4096))
+    return GVX_ERR_INVALID_ARGUMENT;
+  unsigned long long* self = mc_bins ? mc_bins : reinterpret_cast<unsigned long long*>(0x8);  // never dereferenced
+  return mass_histogram_impl(dtype, coords, v1, v2, n, lo, hi, nbins, self, flags, m_out, nullptr, stream,
+                             mc_bins ? nullptr : peer_bins, mc_bins ? 0 : npeers, mc_bins);
+}
+
+static gvx_status mass_histogram_impl(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,
+                                      const gvx_vec4_cview* v2, int64_t n, double lo, double hi, int32_t nbins,
+                                      unsigned long long* bins, uint32_t flags, void* m_out,
+                                      const gvx_vec4_view* boosted_out, gvx_stream_t stream,
+                                      unsigned long long* const* peers, int32_t npeers, unsigned long long* mc) {
   if (!valid_dtype(dtype) || !valid_coords(coords) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
   if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
   if ((flags & ~GVX_HIST_BOOST_TO_CM) != 0u) return GVX_ERR_INVALID_ARGUMENT;
@@ -745,7 +771,10 @@ gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4
   if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !bins || !aligned(bins, 8)) return GVX_ERR_INVALID_ARGUMENT;
   if (m_out && !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
   if (boosted_out && !out_view_ok(boosted_out, es)) return GVX_ERR_INVALID_ARGUMENT;
-  const HistParams hp = make_hist_params(lo, hi, nbins);
+  HistParams hp = make_hist_params(lo, hi, nbins);
+  hp.peers = peers;
+  hp.npeers = npeers;
+  hp.mc = mc;
   cudaStream_t s = (cudaStream_t)stream;
 #define GVX_HIST_DISPATCH(T, C)                                                                                  \
   (cm ? dispatch_hist<T, C, true>(v1, v2, n, hp, bins, m_out, boosted_out, s)                       \

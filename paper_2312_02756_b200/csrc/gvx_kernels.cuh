@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
   auto count = [&](T M) {
     int b = find_bin(M, hp);
     if constexpr (SMEM) atomicAdd(&sh[b], 1u);
-    else atomicAdd(&bins[b], 1ull);
+    else hist_flush(bins, hp, b, 1ull);
   };
   const int64_t ngroups = n / G;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
     __syncthreads();
     for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
       unsigned int c = sh[b];
-      if (c) atomicAdd(&bins[b], (unsigned long long)c);
+      if (c) hist_flush(bins, hp, b, c);
     }
   }
 }
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(256) k_cm_costheta(View4<T> v1, View4<T> v2, i
       atomicAdd(&shc[bm], 1u);
       atomicAdd(&shc[nm + bc], 1u);
     } else {
-      atomicAdd(&mbins[bm], 1ull);
+      hist_flush(mbins, hm, bm, 1ull);
       atomicAdd(&cbins[bc], 1ull);
     }
     if (m_out) m_out[i] = M;
@@ -368,7 +368,10 @@ __global__ void __launch_bounds__(256) k_cm_costheta(View4<T> v1, View4<T> v2, i
     __syncthreads();
     for (int b = threadIdx.x; b < nm + nc; b += blockDim.x) {
       unsigned int v = shc[b];
-      if (v) atomicAdd(b < nm ? &mbins[b] : &cbins[b - nm], (unsigned long long)v);
+      if (v) {
+        if (b < nm) hist_flush(mbins, hm, b, v);
+        else atomicAdd(&cbins[b - nm], (unsigned long long)v);
+      }
     }
   }
 }
@@ -447,7 +450,7 @@ __global__ void __launch_bounds__(256) k_dimuon_histogram(View4<T> mu, const int
   __syncthreads();
   for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
     unsigned int c = shd[b];
-    if (c) atomicAdd(&bins[b], (unsigned long long)c);
+    if (c) hist_flush(bins, hp, b, c);
   }
 }
 
@@ -557,7 +560,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_compact(View4<T> mu, const 
   }
   for (int b = tid; b < nb2; b += NT) {
     const unsigned int c = s_hist[b];
-    if (c) atomicAdd(&bins[b], (unsigned long long)c);
+    if (c) hist_flush(bins, hp, b, c);
   }
 }
 
@@ -713,7 +716,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
   __syncthreads();
   for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
     unsigned int c = sh_hist[b];
-    if (c) atomicAdd(&bins[b], (unsigned long long)c);
+    if (c) hist_flush(bins, hp, b, c);
   }
 }
 
@@ -951,7 +954,10 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
     __syncthreads();
     for (int b = threadIdx.x; b < nbt; b += blockDim.x) {
       unsigned int c = sh_hist[b];
-      if (c) atomicAdd(b < nb2 ? &bins[b] : &co.bins[b - nb2], (unsigned long long)c);
+      if (c) {
+        if (b < nb2) hist_flush(bins, hp, b, c);
+        else atomicAdd(&co.bins[b - nb2], (unsigned long long)c);
+      }
     }
   }
 }

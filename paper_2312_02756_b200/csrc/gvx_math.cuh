@@ -754,6 +754,12 @@ struct HistParams {
   // fp32 masses (find_bin(float)): the same scheme in FP32 with a wider near-edge window
   float lo_f, scale_f, near_f;
   int f32_ok;            // nbins <= 2^20 and the float parameters are finite
+  // Where a CTA's final counts go (hist_flush): the caller's `bins` (default), or
+  // fused into the multi-GPU reduction: every rank's bins through
+  // peer pointers (P2P atomics over NVLink), or one NVSwitch multicast address.
+  unsigned long long* const* peers;  // device array of npeers bin arrays, or NULL
+  int npeers;
+  unsigned long long* mc;            // multicast address of the bins (multimem.red), or NULL
 };
 
 inline HistParams make_hist_params(double lo, double hi, int nbins) {
@@ -776,7 +782,22 @@ inline HistParams make_hist_params(double lo, double hi, int nbins) {
   hp.near_f = (float)(4.0 * (1.8e-7 * (hp.nbins_d + 1.0) + lo_err) + 1e-30);
   hp.f32_ok = nbins <= (1 << 20) && isfinite(hp.lo_f) && isfinite(hp.scale_f) && hp.scale_f > 0.f &&
               hp.near_f < 0.25f;
+  hp.peers = nullptr;
+  hp.npeers = 0;
+  hp.mc = nullptr;
   return hp;
+}
+
+// Add count c to bin b of the histogram described by hp (see HistParams).
+__device__ __forceinline__ void hist_flush(unsigned long long* bins, const HistParams& hp, int b,
+                                           unsigned long long c) {
+  if (hp.mc) {
+    asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(hp.mc + b), "l"(c) : "memory");
+  } else if (hp.npeers > 0) {
+    for (int p = 0; p < hp.npeers; ++p) atomicAdd_system(hp.peers[p] + b, c);
+  } else {
+    atomicAdd(bins + b, c);
+  }
 }
 
 __device__ __noinline__ int find_bin_exact(double x, const HistParams& hp) {

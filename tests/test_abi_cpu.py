@@ -105,6 +105,20 @@ def test_cm_costheta_validation(gvx):
     assert call(n=0, m=(1.0, 1.0, 10)) == 1               # ... but a bad axis is still an error
 
 
+def test_mass_histogram_peers_validation(gvx):
+    """The fused-reduction entry point (ABI v4) checks its sink arguments synchronously."""
+    L = gvx.lib
+    by = ctypes.byref
+    a, b = _view(), _view()
+    P = L.gvx_mass_histogram_peers
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, None, 2, None, 0, None, None) == 1     # no peers
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 0, None, 0, None, None) == 1   # npeers < 1
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, 0x4004, 2, None, 0, None, None) == 1   # misaligned
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, None, 0, 0x5001, 0, None, None) == 1   # misaligned mc
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 1.0, 1.0, 10, 0x4000, 2, None, 0, None, None) == 1   # bad axis
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 0, 0.0, 1.0, 10, 0x4000, 2, None, 0, None, None) == 0   # n == 0
+
+
 def test_lorentz_matrix_validation(gvx):
     """gvx_lorentz_transform checks L^T g L = g on the host before anything is enqueued."""
     L = gvx.lib

@@ -4,6 +4,8 @@ element, on the same seeded inputs. Run on a B200 with ``pytest -m gpu``.
 Inputs come from synth (host generator for the oracle; its bit-identical device
 twin for large batches). No expected value here is produced by the CUDA path.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -893,3 +895,60 @@ def test_dimuon_1e8_full_size(gvx, O):
         assert s == 1
         _, e = O.invariant_mass(hm[:1], hm[1:2])
         assert mass_violations(host(m_out[int(e0):int(e0) + 1]), mo, e, 1e-12).size == 0
+
+
+# ----------------------------------------------------------------------------
+# Cross-GPU bin reduction fused into the kernel tail
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("cm", [False, True])
+def test_mass_histogram_peers_simulated(gvx, dt, cm):
+    """gvx_mass_histogram_peers adds every CTA's counts to each array of the peer list: with
+    three 'peers' that are local buffers, each receives the whole histogram (what every rank of
+    an all-reduce receives), bit-equal to the plain fused histogram, for the TMA ring (AoS),
+    the register kernel (strided pairs) and several launches' worth of accumulation."""
+    import synth.device as sd
+    n = 3 * 1024 * 148 + 77
+    v1, v2 = sd.muon_pairs(n, dtype=TDT[dt])
+    ref = gvx.mass_histogram(v1, v2, cm=cm)
+    pr = torch.stack([v1, v2], 1).contiguous()
+    for a, b in ((v1, v2), (pr[:, 0], pr[:, 1])):
+        peers = [gvx.new_bins() for _ in range(3)]
+        ptrs = torch.tensor([t.data_ptr() for t in peers], dtype=torch.int64, device="cuda")
+        gvx.mass_histogram_peers(a, b, ptrs.data_ptr(), 3, cm=cm)
+        torch.cuda.synchronize()
+        for t in peers:
+            assert torch.equal(t, ref)
+        gvx.mass_histogram_peers(a, b, ptrs.data_ptr(), 3, cm=cm)  # accumulates like the plain call
+        torch.cuda.synchronize()
+        assert torch.equal(peers[1], 2 * ref)
+    with pytest.raises(gvx.GvxError):
+        gvx.mass_histogram_peers(v1, v2, 0, 3)
+    with pytest.raises(gvx.GvxError):
+        gvx.mass_histogram_peers(v1, v2, ptrs.data_ptr(), 0)
+
+
+def test_allreduce_mass_histogram_symmetric_memory_world1():
+    """The symmetric-memory plumbing (rendezvous, peer pointer array, device barriers) on a
+    one-rank NCCL group: the fused all-reduce equals the plain histogram."""
+    import subprocess
+    import sys
+    code = r'''
+import os, torch, torch.distributed as dist
+os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER_PORT", "29731")
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+import paper_2312_02756_b200 as gvx, synth.device as sd
+v1, v2 = sd.muon_pairs(1_000_003, dtype=torch.float64)
+for cm in (False, True):
+    ref = gvx.mass_histogram(v1, v2, cm=cm)
+    got = gvx.allreduce_mass_histogram(v1, v2, cm=cm).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref), (cm, (got - ref).abs().sum().item())
+dist.destroy_process_group()
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, PYTHONPATH=root))
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
