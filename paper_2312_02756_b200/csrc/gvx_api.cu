@@ -751,8 +751,8 @@ gvx_status gvx_mass_histogram_peers(gvx_dtype dtype, gvx_coords coords, const gv
                                     unsigned long long* mc_bins, uint32_t flags, void* m_out, gvx_stream_t stream) {
   if (mc_bins ? !aligned(mc_bins, 8) : (!peer_bins || !aligned(peer_bins, 8) || npeers < 1 || npeers > 4096))
     return GVX_ERR_INVALID_ARGUMENT;
-  unsigned long long* self = mc_bins ? mc_bins : reinterpret_cast<unsigned long long*>(0x8);  // never dereferenced
-  return mass_histogram_impl(dtype, coords, v1, v2, n, lo, hi, nbins, self, flags, m_out, nullptr, stream,
+  // the kernels flush through the sink (HistParams peers / mc) and never touch a local `bins`
+  return mass_histogram_impl(dtype, coords, v1, v2, n, lo, hi, nbins, nullptr, flags, m_out, nullptr, stream,
                              mc_bins ? nullptr : peer_bins, mc_bins ? 0 : npeers, mc_bins);
 }
 
@@ -768,7 +768,9 @@ static gvx_status mass_histogram_impl(gvx_dtype dtype, gvx_coords coords, const 
   if (boosted_out && !cm) return GVX_ERR_INVALID_ARGUMENT;
   if (n == 0) return GVX_OK;
   size_t es = dsize(dtype);
-  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !bins || !aligned(bins, 8)) return GVX_ERR_INVALID_ARGUMENT;
+  const bool sink = peers != nullptr || mc != nullptr;  // fused reduction: counts go to the sink, not `bins`
+  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || (!sink && (!bins || !aligned(bins, 8))))
+    return GVX_ERR_INVALID_ARGUMENT;
   if (m_out && !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
   if (boosted_out && !out_view_ok(boosted_out, es)) return GVX_ERR_INVALID_ARGUMENT;
   HistParams hp = make_hist_params(lo, hi, nbins);
