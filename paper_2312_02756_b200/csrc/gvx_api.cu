@@ -324,6 +324,10 @@ gvx_status launch_boost(const gvx_vec4_cview* v, const gvx_vec3_cview* beta, con
     aos = aos && (const char*)v->c[k] == vb + k * sizeof(T) && (const char*)out->c[k] == ob + k * sizeof(T);
   if (aos) {
     auto k = k_boost<T, true, UNI>;
+#ifdef GVX_TUNE
+    if (tune_env("GVX_BOOST_U") == 2) k = k_boost<T, true, UNI, 2>;
+    if (tune_env("GVX_BOOST_U") == 4) k = k_boost<T, true, UNI, 4>;
+#endif
     int grid = grid_for(k, kBlock, 0, kBlock, n);
     k<<<grid, kBlock, 0, s>>>(mk4<T>(v), mk3<T>(beta), mk4o<T>(out), n, bx, by, bz);
   } else {

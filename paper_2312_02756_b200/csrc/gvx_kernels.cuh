@@ -157,43 +157,71 @@ __global__ void __launch_bounds__(256, MINB) k_invariant_mass(View4<T> v1, View4
 // ============================================================================
 // K2: boost by per-event (or uniform) beta
 // ============================================================================
-template <typename T, bool AOS, bool UNIFORM>
+template <typename T, bool AOS>
+__device__ __forceinline__ V4<T> boost_load_v(const View4<T>& v, int64_t i) {
+  if constexpr (AOS) {
+    if constexpr (sizeof(T) == 8) {
+      double r[4];
+      ld256(reinterpret_cast<const double*>(v.c[0]) + 4 * i, r);
+      return V4<T>{(T)r[0], (T)r[1], (T)r[2], (T)r[3]};
+    } else {
+      float4 r = __ldcs(reinterpret_cast<const float4*>(v.c[0]) + i);
+      return V4<T>{(T)r.x, (T)r.y, (T)r.z, (T)r.w};
+    }
+  } else {
+    return V4<T>{__ldg(v.c[0] + i * v.s), __ldg(v.c[1] + i * v.s), __ldg(v.c[2] + i * v.s), __ldg(v.c[3] + i * v.s)};
+  }
+}
+template <typename T, bool AOS>
+__device__ __forceinline__ void boost_store(const View4o<T>& out, int64_t i, const V4<T>& o) {
+  if constexpr (AOS) {
+    if constexpr (sizeof(T) == 8) {
+      double r[4] = {(double)o.x, (double)o.y, (double)o.z, (double)o.t};
+      st256(reinterpret_cast<double*>(out.c[0]) + 4 * i, r);
+    } else {
+      __stcs(reinterpret_cast<float4*>(out.c[0]) + i, make_float4((float)o.x, (float)o.y, (float)o.z, (float)o.t));
+    }
+  } else {
+    out.c[0][i * out.s] = o.x;
+    out.c[1][i * out.s] = o.y;
+    out.c[2][i * out.s] = o.z;
+    out.c[3][i * out.s] = o.t;
+  }
+}
+
+// U events per thread per iteration: all loads issued before any arithmetic
+// (bytes in flight per SM scale with U at the same occupancy).
+template <typename T, bool AOS, bool UNIFORM, int U = 1>
 __global__ void __launch_bounds__(256) k_boost(View4<T> v, View3<T> beta, View4o<T> out, int64_t n, T ubx,
                                                T uby, T ubz) {
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   BoostCoef<T> ku;
   if constexpr (UNIFORM) ku = boost_coef(ubx, uby, ubz);
-  for (int64_t i = tid; i < n; i += nthr) {
-    V4<T> x;
-    if constexpr (AOS) {
-      if constexpr (sizeof(T) == 8) {
-        double r[4];
-        ld256(reinterpret_cast<const double*>(v.c[0]) + 4 * i, r);
-        x = V4<T>{(T)r[0], (T)r[1], (T)r[2], (T)r[3]};
-      } else {
-        float4 r = __ldcs(reinterpret_cast<const float4*>(v.c[0]) + i);
-        x = V4<T>{(T)r.x, (T)r.y, (T)r.z, (T)r.w};
+  for (int64_t i0 = tid; i0 < n; i0 += nthr * U) {
+    V4<T> x[U];
+    T bx[U], by[U], bz[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * nthr;
+      if (i < n) {
+        x[u] = boost_load_v<T, AOS>(v, i);
+        if constexpr (!UNIFORM) {
+          bx[u] = __ldg(beta.c[0] + i * beta.s);
+          by[u] = __ldg(beta.c[1] + i * beta.s);
+          bz[u] = __ldg(beta.c[2] + i * beta.s);
+        }
       }
-    } else {
-      x = V4<T>{__ldg(v.c[0] + i * v.s), __ldg(v.c[1] + i * v.s), __ldg(v.c[2] + i * v.s), __ldg(v.c[3] + i * v.s)};
     }
-    BoostCoef<T> k;
-    if constexpr (UNIFORM) k = ku;
-    else k = boost_coef(__ldg(beta.c[0] + i * beta.s), __ldg(beta.c[1] + i * beta.s), __ldg(beta.c[2] + i * beta.s));
-    V4<T> o = apply_boost(k, x);
-    if constexpr (AOS) {
-      if constexpr (sizeof(T) == 8) {
-        double r[4] = {(double)o.x, (double)o.y, (double)o.z, (double)o.t};
-        st256(reinterpret_cast<double*>(out.c[0]) + 4 * i, r);
-      } else {
-        __stcs(reinterpret_cast<float4*>(out.c[0]) + i, make_float4((float)o.x, (float)o.y, (float)o.z, (float)o.t));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * nthr;
+      if (i < n) {
+        BoostCoef<T> k;
+        if constexpr (UNIFORM) k = ku;
+        else k = boost_coef(bx[u], by[u], bz[u]);
+        boost_store<T, AOS>(out, i, apply_boost(k, x[u]));
       }
-    } else {
-      out.c[0][i * out.s] = o.x;
-      out.c[1][i * out.s] = o.y;
-      out.c[2][i * out.s] = o.z;
-      out.c[3][i * out.s] = o.t;
     }
   }
 }
