@@ -406,6 +406,13 @@ def run_ours(args):
                 "peak_source": peak_kind,
                 "bytes_per_launch": n * BYTES[dom](es)}
 
+    # K5: the read-only streaming peak measured in this run (one launch over an 8 GB scratch
+    # buffer, 64x L2, freed afterwards)
+    scratch = torch.empty(8 << 30, dtype=torch.uint8, device=dev)
+    read_peak = sd.stream_read_gbs([scratch])
+    del scratch
+    for k in KERNEL_ORDER:
+        kernels[k]["frac_of_read_peak"] = kernels[k]["achieved_GBs"] / read_peak
     extended = run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak) if args.extended else None
 
     # e2e: the same step from pinned HOST buffers through the public API, copies timed
@@ -426,6 +433,10 @@ def run_ours(args):
             "config": config_obj(args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk.summary(), "kernels": kernels,
+            "peaks": {"copy_GBs": peak, "copy_source": peak_kind, "read_stream_GBs": read_peak,
+                      "read_stream_source": "K5 stream-read probe in this run (synth/libgvxsynth.so, 256-bit "
+                                            "non-caching loads over an 8 GB buffer, best of 5)",
+                      "nominal_GBs": 8000.0},
             "step_hbm": {"algorithmic_bytes_per_gpu": step_bytes, "achieved_GBs_per_gpu": step_gbs,
                          "frac_of_peak": step_gbs / peak, "peak": peak},
             **({"extended": extended} if extended else {}),

@@ -30,6 +30,8 @@ def _load():
         lib.gvx_synth_jagged_fill.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         lib.gvx_synth_jagged_fill.restype = ctypes.c_int
+        lib.gvx_synth_stream_read.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        lib.gvx_synth_stream_read.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -89,3 +91,29 @@ def jagged_events(first_event: int, n_events: int, seed: int = DEFAULT_SEED, dty
         if rc:
             raise RuntimeError(f"gvx_synth_jagged_fill: cuda error {rc}")
     return mu, q, offsets
+
+
+def stream_read_gbs(buffers, reps: int = 5) -> float:
+    """K5: achievable HBM read bandwidth, GB/s, of one streaming pass over the
+    given device tensors (each read once per rep; take buffers much larger than L2), CUDA
+    events on the current stream, best of ``reps``."""
+    lib = _load()
+    dev = buffers[0].device
+    sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream(dev)
+    total = 0
+    for b in buffers:
+        total += (b.numel() * b.element_size()) // 32 * 32
+    best = float("inf")
+    for _ in range(reps + 1):
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for b in buffers:
+            rc = lib.gvx_synth_stream_read(b.data_ptr(), b.numel() * b.element_size(), sink.data_ptr(),
+                                           st.cuda_stream)
+            if rc != 0:
+                raise RuntimeError(f"gvx_synth_stream_read: cuda error {rc}")
+        z.record(st)
+        z.synchronize()
+        best = min(best, a.elapsed_time(z))
+    return total / (best * 1e-3) / 1e9

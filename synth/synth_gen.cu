@@ -117,6 +117,27 @@ __global__ void k_jagged_fill(uint64_t seed, uint64_t first, int64_t n, const in
   }
 }
 
+// K5: read-only streaming probe for the achievable HBM read
+// bandwidth in the same run as the measurements it normalises. Persistent
+// grid of 4 x 512-thread CTAs per SM (the best geometry of the pool probe,
+// profiles/r01_hwprobe.jsonl: 7.29 TB/s), one 256-bit non-caching load per
+// thread per iteration, XOR-folded so the loads cannot be elided.
+__global__ void __launch_bounds__(512) k_stream_read(const double4* __restrict__ p, int64_t n4,
+                                                     unsigned long long* __restrict__ sink) {
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += nthr) {
+    double r0, r1, r2, r3;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r0), "=d"(r1), "=d"(r2), "=d"(r3)
+                 : "l"(p + i));
+    acc ^= (unsigned long long)__double_as_longlong(r0) ^ (unsigned long long)__double_as_longlong(r1) ^
+           (unsigned long long)__double_as_longlong(r2) ^ (unsigned long long)__double_as_longlong(r3);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicXor(sink, acc);
+}
+
 int grid_of(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
@@ -160,6 +181,18 @@ int gvx_synth_jagged_fill(int dtype, uint64_t seed, uint64_t first, int64_t n, c
     k_jagged_fill<double><<<grid_of(n), 256, 0, s>>>(seed, first, n, (const int64_t*)offsets, (double*)mu, (int32_t*)q);
   else
     k_jagged_fill<float><<<grid_of(n), 256, 0, s>>>(seed, first, n, (const int64_t*)offsets, (float*)mu, (int32_t*)q);
+  return (int)cudaGetLastError();
+}
+
+// K5: stream `bytes` (multiple of 32, 32-byte aligned) of device memory once; the
+// XOR of all words lands in *sink (8 bytes of device memory).
+int gvx_synth_stream_read(const void* buf, int64_t bytes, void* sink, void* stream) {
+  if (bytes < 32) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_stream_read<<<sms * 4, 512, 0, (cudaStream_t)stream>>>((const double4*)buf, bytes / 32,
+                                                           (unsigned long long*)sink);
   return (int)cudaGetLastError();
 }
 
