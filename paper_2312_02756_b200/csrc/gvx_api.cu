@@ -178,8 +178,11 @@ bool tma_preferred() {
 // consumers need warps (FP64 latency) more than ring depth.
 template <typename T, int MODE> struct TmaCfgOf;
 template <int MODE> struct TmaCfgOf<double, MODE> { using type = PairTma<double, 896, 2, 28, 1>; };
-template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 992, 3, 31, 1>; };
-template <> struct TmaCfgOf<double, PM_HIST_CM_COS> { using type = PairTma<double, 992, 3, 31, 1>; };
+// fp64 CM: 24 consumer warps x 2 events each, run as two interleaved chains
+// (pair_consume_x2): 1.16 vs 1.24 ms for 31 warps x 1 event
+// (profiles/r01/sweep_f64_cm_x2.jsonl).
+template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 1536, 2, 24, 1>; };
+template <> struct TmaCfgOf<double, PM_HIST_CM_COS> { using type = PairTma<double, 1536, 2, 24, 1>; };
 template <int MODE> struct TmaCfgOf<float, MODE> { using type = PairTma<float, 896, 4, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM> { using type = PairTma<float, 1792, 3, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM_COS> { using type = PairTma<float, 1792, 3, 28, 1>; };
@@ -254,6 +257,12 @@ gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, i
       case 11: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 896, 2, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       case 12: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1024, 3, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       case 13: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1280, 2, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 14: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1536, 2, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 15: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1664, 2, 26, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 16: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1408, 2, 22, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 17: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1152, 3, 18, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 18: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1536, 2, 12, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 19: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1536, 2, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       default: break;
     }
   }

@@ -852,6 +852,43 @@ __device__ __forceinline__ void pair_consume_x2(const float (&a0)[4], const floa
   }
 }
 
+// fp64 CM modes, two events of a thread in one branch-free block (both in the
+// fast domain): the two independent dependency chains give the scheduler ILP
+// on the FP64 pipe. Same arithmetic as the one-event path (bit-identical).
+template <int COORDS, int MODE>
+__device__ __forceinline__ void pair_consume_x2(const double (&a0)[4], const double (&b0)[4], const double (&a1)[4],
+                                                const double (&b1)[4], int64_t i0, int64_t i1,
+                                                double* __restrict__ m_out, unsigned int* sh_hist,
+                                                const HistParams& hp, const View4o<double>& bo, unsigned int* sh_cos,
+                                                const CosOut<double>& co) {
+  if (fast_domain(a0[0], a0[1], a0[2], a0[3]) & fast_domain(b0[0], b0[1], b0[2], b0[3]) &
+      fast_domain(a1[0], a1[1], a1[2], a1[3]) & fast_domain(b1[0], b1[1], b1[2], b1[3])) {
+    constexpr bool COS = MODE == PM_HIST_CM_COS;
+    double c0, c1;
+    const double M0 = cm_mass_ptetaphim_fast<double, COS>(a0[0], a0[1], a0[2], a0[3], b0[0], b0[1], b0[2], b0[3],
+                                                          nullptr, nullptr, &c0);
+    const double M1 = cm_mass_ptetaphim_fast<double, COS>(a1[0], a1[1], a1[2], a1[3], b1[0], b1[1], b1[2], b1[3],
+                                                          nullptr, nullptr, &c1);
+    atomicAdd(&sh_hist[find_bin(M0, hp)], 1u);
+    atomicAdd(&sh_hist[find_bin(M1, hp)], 1u);
+    if (m_out) {
+      m_out[i0] = M0;
+      m_out[i1] = M1;
+    }
+    if constexpr (COS) {
+      atomicAdd(&sh_cos[find_bin(c0, co.hc)], 1u);
+      atomicAdd(&sh_cos[find_bin(c1, co.hc)], 1u);
+      if (co.cos_out) {
+        co.cos_out[i0] = c0;
+        co.cos_out[i1] = c1;
+      }
+    }
+  } else {
+    pair_consume<double, COORDS, MODE, false>(a0, b0, i0, m_out, sh_hist, hp, bo, sh_cos, co);
+    pair_consume<double, COORDS, MODE, false>(a1, b1, i1, m_out, sh_hist, hp, bo, sh_cos, co);
+  }
+}
+
 // SOA = false: each stage holds the v1 and v2 AoS tiles (2 bulk copies);
 // SOA = true: the 8 component tiles of v1 and v2 (8 bulk copies), read back
 // lane-contiguously (LDS.64 / LDS.32, no bank conflicts).
@@ -947,8 +984,8 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
 #endif
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
-      constexpr bool PACK = sizeof(T) == 4 && (MODE == PM_HIST_CM || MODE == PM_HIST_CM_COS) &&
-                            COORDS == C_PTETAPHIM && !WANT_BO && CFG::EPT % 2 == 0;
+      constexpr bool PACK = (MODE == PM_HIST_CM || MODE == PM_HIST_CM_COS) && COORDS == C_PTETAPHIM && !WANT_BO &&
+                            CFG::EPT % 2 == 0;
       if constexpr (PACK) {
 #pragma unroll
         for (int u = 0; u < CFG::EPT; u += 2)
