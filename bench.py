@@ -434,8 +434,8 @@ def run_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk.summary(), "kernels": kernels,
             "peaks": {"copy_GBs": peak, "copy_source": peak_kind, "read_stream_GBs": read_peak,
-                      "read_stream_source": "K5 stream-read probe in this run (synth/libgvxsynth.so, 256-bit "
-                                            "non-caching loads over an 8 GB buffer, best of 5)",
+                      "read_stream_source": "K5 stream-read probe in this run (synth/libgvxsynth.so: TMA bulk-copy "
+                                            "ring, 6 x 16 KB stages per SM, over an 8 GB buffer, best of 5)",
                       "nominal_GBs": 8000.0},
             "step_hbm": {"algorithmic_bytes_per_gpu": step_bytes, "achieved_GBs_per_gpu": step_gbs,
                          "frac_of_peak": step_gbs / peak, "peak": peak},
@@ -477,6 +477,12 @@ def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
         # f2: CM mass + cos θ* histograms in one pass (reading R22)
         "cm_costheta_hist": (lambda: gvx.cm_costheta_histogram(v1, v2), 8 * es),
     }
+    # single-bin stress: every pair at rest with M = 91 GeV (PxPyPzE (0, 0, 0, 45.5)
+    # twice), so all events of a CTA hit one shared-memory counter — worst-case atomic contention
+    rest = torch.zeros((n, 4), dtype=v1.dtype, device=v1.device)
+    rest[:, 3] = 45.5
+    rest2 = rest.clone()  # a distinct array: both vectors of a pair stream from HBM
+    cases["hist_single_bin_stress"] = (lambda: gvx.mass_histogram(rest, rest2, coords="pxpypze"), 8 * es)
     # jagged events (f4): 1 event per pair slot of the batch, ~1.1 muons/event on average
     import synth.device as sd
     jmu, jq, joff = sd.jagged_events(0, n, dtype=v1.dtype, device=v1.device)
@@ -497,7 +503,8 @@ def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
     out["dimuon_jagged"]["selected_events"] = n_sel
     out["dimuon_jagged"]["note"] = ("bytes/event = offsets + charges of 2-muon events + kinematics of "
                                     "selected events (algorithmic)")
-    del s1, s2, jmu, jq, joff
+    out["hist_single_bin_stress"]["note"] = "all pairs in one bin (PxPyPzE at rest, M = 91 GeV): atomic contention"
+    del s1, s2, jmu, jq, joff, rest, rest2
     return out
 
 

@@ -103,7 +103,7 @@ def stream_read_gbs(buffers, reps: int = 5) -> float:
     st = torch.cuda.current_stream(dev)
     total = 0
     for b in buffers:
-        total += (b.numel() * b.element_size()) // 32 * 32
+        total += (b.numel() * b.element_size()) // 16384 * 16384  # whole 16-KB tiles
     best = float("inf")
     for _ in range(reps + 1):
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

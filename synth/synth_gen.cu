@@ -118,24 +118,74 @@ __global__ void k_jagged_fill(uint64_t seed, uint64_t first, int64_t n, const in
 }
 
 // K5: read-only streaming probe for the achievable HBM read
-// bandwidth in the same run as the measurements it normalises. Persistent
-// grid of 4 x 512-thread CTAs per SM (the best geometry of the pool probe,
-// profiles/r01_hwprobe.jsonl: 7.29 TB/s), one 256-bit non-caching load per
-// thread per iteration, XOR-folded so the loads cannot be elided.
-__global__ void __launch_bounds__(512) k_stream_read(const double4* __restrict__ p, int64_t n4,
-                                                     unsigned long long* __restrict__ sink) {
-  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  unsigned long long acc = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += nthr) {
-    double r0, r1, r2, r3;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(r0), "=d"(r1), "=d"(r2), "=d"(r3)
-                 : "l"(p + i));
-    acc ^= (unsigned long long)__double_as_longlong(r0) ^ (unsigned long long)__double_as_longlong(r1) ^
-           (unsigned long long)__double_as_longlong(r2) ^ (unsigned long long)__double_as_longlong(r3);
+// bandwidth in the same run as the measurements it normalises: a bulk-copy
+// (cp.async.bulk, TMA) ring, one CTA per SM, 6 stages of 16 KB, one producer
+// lane, 8 consumer warps that read every 16 B of a stage (LDS.128 + xor) and
+// release it — the best geometry of the pool probe (profiles/r01/tmaprobe.jsonl,
+// 7.35-7.49 TB/s). Self-contained PTX (no product header).
+namespace k5 {
+constexpr int STAGE = 16384, STAGES = 6, NCW = 8;
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(sa(bar)), "r"(parity) : "memory");
+}
+}  // namespace k5
+
+__global__ void __launch_bounds__(32 * (k5::NCW + 1)) k_stream_read(const char* __restrict__ src, int64_t ntiles,
+                                                                   unsigned long long* __restrict__ sink) {
+  using namespace k5;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&full[s])), "r"(1) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&empty[s])), "r"(NCW) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) atomicXor(sink, acc);
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it % STAGES, k = it / STAGES;
+        if (k > 0) {
+          wait(&empty[s], (k - 1) & 1);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(STAGE)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+            ::"r"(sa(smem + s * STAGE)), "l"(src + t * STAGE), "r"(STAGE), "r"(sa(&full[s])), "l"(pol)
+            : "memory");
+      }
+    }
+  } else {
+    unsigned long long acc = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int s = it % STAGES, k = it / STAGES;
+      wait(&full[s], k & 1);
+      const int4* p = reinterpret_cast<const int4*>(smem + s * STAGE);
+      for (int i = threadIdx.x - 32; i < STAGE / 16; i += NCW * 32) {
+        const int4 v = p[i];
+        acc ^= (unsigned long long)(unsigned)(v.x ^ v.y ^ v.z ^ v.w);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[s])) : "memory");
+    }
+    for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) atomicXor(sink, acc);
+  }
 }
 
 int grid_of(int64_t n) {
@@ -184,15 +234,18 @@ int gvx_synth_jagged_fill(int dtype, uint64_t seed, uint64_t first, int64_t n, c
   return (int)cudaGetLastError();
 }
 
-// K5: stream `bytes` (multiple of 32, 32-byte aligned) of device memory once; the
-// XOR of all words lands in *sink (8 bytes of device memory).
+// K5: stream `bytes` (the whole 16-KB tiles of it; 16-byte aligned) of device
+// memory once; the XOR of the data lands in *sink (8 bytes of device memory).
 int gvx_synth_stream_read(const void* buf, int64_t bytes, void* sink, void* stream) {
-  if (bytes < 32) return 0;
+  const int64_t ntiles = bytes / k5::STAGE;
+  if (ntiles < 1) return 0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  k_stream_read<<<sms * 4, 512, 0, (cudaStream_t)stream>>>((const double4*)buf, bytes / 32,
-                                                           (unsigned long long*)sink);
+  const int smem = k5::STAGES * k5::STAGE + 2 * k5::STAGES * 8;
+  cudaFuncSetAttribute(k_stream_read, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_stream_read<<<sms, 32 * (k5::NCW + 1), smem, (cudaStream_t)stream>>>((const char*)buf, ntiles,
+                                                                        (unsigned long long*)sink);
   return (int)cudaGetLastError();
 }
 
