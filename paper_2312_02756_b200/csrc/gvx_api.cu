@@ -182,6 +182,8 @@ template <int MODE> struct TmaCfgOf<double, MODE> { using type = PairTma<double,
 // (pair_consume_x2): 1.16 vs 1.24 ms for 31 warps x 1 event
 // (profiles/r01/sweep_f64_cm_x2.jsonl).
 template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 1536, 2, 24, 1>; };
+// fp64 lab histogram: 20 warps x 2 interleaved events, 0.904 vs 0.934 ms (same sweep)
+template <> struct TmaCfgOf<double, PM_HIST> { using type = PairTma<double, 1280, 2, 20, 1>; };
 template <> struct TmaCfgOf<double, PM_HIST_CM_COS> { using type = PairTma<double, 1536, 2, 24, 1>; };
 template <int MODE> struct TmaCfgOf<float, MODE> { using type = PairTma<float, 896, 4, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM> { using type = PairTma<float, 1792, 3, 28, 1>; };

@@ -864,11 +864,22 @@ __device__ __forceinline__ void pair_consume_x2(const double (&a0)[4], const dou
   if (fast_domain(a0[0], a0[1], a0[2], a0[3]) & fast_domain(b0[0], b0[1], b0[2], b0[3]) &
       fast_domain(a1[0], a1[1], a1[2], a1[3]) & fast_domain(b1[0], b1[1], b1[2], b1[3])) {
     constexpr bool COS = MODE == PM_HIST_CM_COS;
-    double c0, c1;
-    const double M0 = cm_mass_ptetaphim_fast<double, COS>(a0[0], a0[1], a0[2], a0[3], b0[0], b0[1], b0[2], b0[3],
-                                                          nullptr, nullptr, &c0);
-    const double M1 = cm_mass_ptetaphim_fast<double, COS>(a1[0], a1[1], a1[2], a1[3], b1[0], b1[1], b1[2], b1[3],
-                                                          nullptr, nullptr, &c1);
+    constexpr bool LAB = MODE == PM_MASS || MODE == PM_HIST;
+    double c0, c1, M0, M1;
+    if constexpr (LAB) {
+      M0 = pair_mass_fast(a0[0], a0[1], a0[2], a0[3], b0[0], b0[1], b0[2], b0[3]);
+      M1 = pair_mass_fast(a1[0], a1[1], a1[2], a1[3], b1[0], b1[1], b1[2], b1[3]);
+      if constexpr (MODE == PM_MASS) {
+        m_out[i0] = M0;
+        m_out[i1] = M1;
+        return;
+      }
+    } else {
+      M0 = cm_mass_ptetaphim_fast<double, COS>(a0[0], a0[1], a0[2], a0[3], b0[0], b0[1], b0[2], b0[3], nullptr,
+                                               nullptr, &c0);
+      M1 = cm_mass_ptetaphim_fast<double, COS>(a1[0], a1[1], a1[2], a1[3], b1[0], b1[1], b1[2], b1[3], nullptr,
+                                               nullptr, &c1);
+    }
     atomicAdd(&sh_hist[find_bin(M0, hp)], 1u);
     atomicAdd(&sh_hist[find_bin(M1, hp)], 1u);
     if (m_out) {
@@ -888,6 +899,7 @@ __device__ __forceinline__ void pair_consume_x2(const double (&a0)[4], const dou
     pair_consume<double, COORDS, MODE, false>(a1, b1, i1, m_out, sh_hist, hp, bo, sh_cos, co);
   }
 }
+
 
 // SOA = false: each stage holds the v1 and v2 AoS tiles (2 bulk copies);
 // SOA = true: the 8 component tiles of v1 and v2 (8 bulk copies), read back
@@ -984,8 +996,9 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
 #endif
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
-      constexpr bool PACK = (MODE == PM_HIST_CM || MODE == PM_HIST_CM_COS) && COORDS == C_PTETAPHIM && !WANT_BO &&
-                            CFG::EPT % 2 == 0;
+      // two events per call: packed FP32 for the f32 CM modes, two interleaved FP64 chains for f64
+      constexpr bool PACK = COORDS == C_PTETAPHIM && !WANT_BO && CFG::EPT % 2 == 0 &&
+                            (MODE == PM_HIST_CM || MODE == PM_HIST_CM_COS || sizeof(T) == 8);
       if constexpr (PACK) {
 #pragma unroll
         for (int u = 0; u < CFG::EPT; u += 2)
