@@ -535,12 +535,15 @@ gvx_status launch_dimuon_tma(const gvx_vec4_cview* mu, const int32_t* q, const i
 // Stream-compacted dimuon kernel (default): ET events per tile, NT threads.
 // Default geometry from the B200 sweep (profiles/r01/sweep_dimuon_compact.jsonl):
 // 2048-event tiles, 256 threads, 5 CTAs/SM (MINB 5 caps registers at 48).
-template <typename T, bool AOS, int ET = 2048, int NT = 256, int MINB = 5>
+template <typename T, bool AOS, int ET = 2048, int NT = 256, int MINB = 5, int U = 1>
 gvx_status launch_dimuon_compact(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
                                  const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
 #ifdef GVX_TUNE
-  if constexpr (ET == 2048 && NT == 256 && MINB == 5) {
+  if constexpr (ET == 2048 && NT == 256 && MINB == 5 && U == 1) {
     switch (tune_env("GVX_DIMUON_CFG")) {
+      case 7: return launch_dimuon_compact<T, AOS, 2048, 256, 5, 2>(mu, q, off, n_events, hp, bins, m_out, s);
+      case 8: return launch_dimuon_compact<T, AOS, 2048, 256, 4, 2>(mu, q, off, n_events, hp, bins, m_out, s);
+      case 9: return launch_dimuon_compact<T, AOS, 2048, 256, 3, 2>(mu, q, off, n_events, hp, bins, m_out, s);
       case 1: return launch_dimuon_compact<T, AOS, 2048, 256, 4>(mu, q, off, n_events, hp, bins, m_out, s);
       case 2: return launch_dimuon_compact<T, AOS, 2048, 256, 6>(mu, q, off, n_events, hp, bins, m_out, s);
       case 3: return launch_dimuon_compact<T, AOS, 1024, 256, 4>(mu, q, off, n_events, hp, bins, m_out, s);
@@ -553,7 +556,7 @@ gvx_status launch_dimuon_compact(const gvx_vec4_cview* mu, const int32_t* q, con
 #endif
   const size_t sm = dimuon_compact_smem<ET>(hp.nbins + 2);
   if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
-  auto k = k_dimuon_compact<T, AOS, ET, NT, 1, MINB>;
+  auto k = k_dimuon_compact<T, AOS, ET, NT, U, MINB>;
   const int grid = grid_for(k, NT, sm, ET, n_events);
   // uint32 shared-memory bins: one launch covers at most grid * 2^31 events
   const int64_t chunk = (int64_t)grid << 31;
