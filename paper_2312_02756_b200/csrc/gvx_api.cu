@@ -280,6 +280,12 @@ gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, i
     }
   }
 #endif
+  if constexpr (sizeof(T) == 4 && MODE == PM_HIST) {
+    // SoA views: 8 component copies per stage; the 2-event packed ring measured faster there
+    // (0.455 vs 0.496 ms at 1e8, profiles/r01/sweep_f32_lab_packed.jsonl)
+    if (classify(v1, sizeof(T)) == L_SOA && classify(v2, sizeof(T)) == L_SOA)
+      return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1792, 3, 28, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+  }
   return launch_pair_tma_cfg<T, C, MODE, typename TmaCfgOf<T, MODE>::type>(v1, v2, n, m_out, hp, bins, bo, s, co);
 }
 

@@ -828,10 +828,20 @@ __device__ __forceinline__ void pair_consume_x2(const float (&a0)[4], const floa
       fast_domain(a1[0], a1[1], a1[2], a1[3]) & fast_domain(b1[0], b1[1], b1[2], b1[3])) {
     constexpr bool COS = MODE == PM_HIST_CM_COS;
     float2 c;
-    const float2 M = cm_mass_f32_lanes<float2, COS, false>(
-        make_float2(a0[0], a1[0]), make_float2(a0[1], a1[1]), make_float2(a0[2], a1[2]), make_float2(a0[3], a1[3]),
-        make_float2(b0[0], b1[0]), make_float2(b0[1], b1[1]), make_float2(b0[2], b1[2]), make_float2(b0[3], b1[3]),
-        &c, nullptr);
+    const float2 A0 = make_float2(a0[0], a1[0]), A1 = make_float2(a0[1], a1[1]), A2 = make_float2(a0[2], a1[2]),
+                 A3 = make_float2(a0[3], a1[3]), B0 = make_float2(b0[0], b1[0]), B1 = make_float2(b0[1], b1[1]),
+                 B2 = make_float2(b0[2], b1[2]), B3 = make_float2(b0[3], b1[3]);
+    float2 M;
+    if constexpr (MODE == PM_MASS || MODE == PM_HIST) {
+      M = pair_mass_f32_lanes<float2>(A0, A1, A2, A3, B0, B1, B2, B3);
+      if constexpr (MODE == PM_MASS) {
+        m_out[i0] = M.x;
+        m_out[i1] = M.y;
+        return;
+      }
+    } else {
+      M = cm_mass_f32_lanes<float2, COS, false>(A0, A1, A2, A3, B0, B1, B2, B3, &c, nullptr);
+    }
     atomicAdd(&sh_hist[find_bin(M.x, hp)], 1u);
     atomicAdd(&sh_hist[find_bin(M.y, hp)], 1u);
     if (m_out) {
@@ -997,8 +1007,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
       // two events per call: packed FP32 for the f32 CM modes, two interleaved FP64 chains for f64
-      constexpr bool PACK = COORDS == C_PTETAPHIM && !WANT_BO && CFG::EPT % 2 == 0 &&
-                            (MODE == PM_HIST_CM || MODE == PM_HIST_CM_COS || sizeof(T) == 8);
+      constexpr bool PACK = COORDS == C_PTETAPHIM && !WANT_BO && CFG::EPT % 2 == 0;
       if constexpr (PACK) {
 #pragma unroll
         for (int u = 0; u < CFG::EPT; u += 2)

@@ -324,21 +324,15 @@ __device__ __forceinline__ float reduce_2pi(float d) {
   return fmaf(-k, TWO_PI_LO, r);
 }
 
+template <typename V>
+__device__ __forceinline__ V pair_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt2, V eta2, V phi2, V m2);
+
+// fp32 lab mass: the lane-generic form (pair_mass_f32_lanes, defined with the
+// lane helpers below) so the packed two-event path of the TMA kernels gives
+// the same bits as this scalar one.
 __device__ __forceinline__ float pair_mass_fast(float pt1, float eta1, float phi1, float m1, float pt2, float eta2,
                                                 float phi2, float m2) {
-  const float LOG2E = 1.44269504088896341f;
-  float c = __cosf(reduce_2pi(phi1 - phi2));
-  float e1 = fast_ex2(eta1 * LOG2E), e2 = fast_ex2(eta2 * LOG2E);
-  float r1 = fast_rcp(e1), r2 = fast_rcp(e2);
-  float sh1 = 0.5f * (e1 - r1), ch1 = 0.5f * (e1 + r1);
-  float sh2 = 0.5f * (e2 - r2), ch2 = 0.5f * (e2 + r2);
-  float q1 = pt1 * ch1, q2 = pt2 * ch2;
-  float P1 = q1 * q1, P2 = q2 * q2;
-  float mm1 = m1 * fabsf(m1), mm2 = m2 * fabsf(m2);
-  float E1 = fast_sqrt(fmaxf(mm1 + P1, 0.f)), E2 = fast_sqrt(fmaxf(mm2 + P2, 0.f));
-  float t = fmaxf(mm1, -P1) + fmaxf(mm2, -P2);
-  float m2sq = t + 2.f * (E1 * E2 - pt1 * pt2 * (c + sh1 * sh2));
-  return m2sq >= 0.f ? fast_sqrt(m2sq) : -fast_sqrt(-m2sq);
+  return pair_mass_f32_lanes<float>(pt1, eta1, phi1, m1, pt2, eta2, phi2, m2);
 }
 
 template <typename T>
@@ -610,6 +604,38 @@ template <typename F> __device__ __forceinline__ float2 lv_map(float2 a, F f) { 
 template <typename F> __device__ __forceinline__ float lv_map2(float a, float b, F f) { return f(a, b); }
 template <typename F> __device__ __forceinline__ float2 lv_map2(float2 a, float2 b, F f) {
   return make_float2(f(a.x, b.x), f(a.y, b.y));
+}
+
+// fp32 lab pair mass (reduced form of pair_mass_fast(double), MUFU functions):
+//   M^2 = t1 + t2 + 2 (E1 E2 - pt1 pt2 (cos(phi1 - phi2) + sinh eta1 sinh eta2)),
+// every product-feeding sum an explicit fma (see cm_mass_f32_lanes).
+template <typename V>
+__device__ __forceinline__ V pair_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt2, V eta2, V phi2, V m2) {
+  const V MONE = lv_splat(V{}, -1.f), HALF = lv_splat(V{}, 0.5f), TWO = lv_splat(V{}, 2.f);
+  const V LOG2E = lv_splat(V{}, 1.44269504088896341f);
+  V d = lv_fma(phi2, MONE, phi1);
+  V k = lv_map(lv_mul(d, lv_splat(V{}, 0.159154943091895336f)), [](float x) { return rintf(x); });
+  V r = lv_fma(k, lv_splat(V{}, -6.28318548202514648f), d);
+  r = lv_fma(k, lv_splat(V{}, 1.74845553146951715e-7f), r);
+  V c = lv_map(r, [](float x) { return __cosf(x); });
+  V e1 = lv_map(lv_mul(eta1, LOG2E), [](float x) { return fast_ex2(x); });
+  V e2 = lv_map(lv_mul(eta2, LOG2E), [](float x) { return fast_ex2(x); });
+  V r1 = lv_map(e1, [](float x) { return fast_rcp(x); }), r2 = lv_map(e2, [](float x) { return fast_rcp(x); });
+  V sh1 = lv_mul(lv_fma(r1, MONE, e1), HALF), ch1 = lv_mul(lv_add(e1, r1), HALF);
+  V sh2 = lv_mul(lv_fma(r2, MONE, e2), HALF), ch2 = lv_mul(lv_add(e2, r2), HALF);
+  V q1 = lv_mul(pt1, ch1), q2 = lv_mul(pt2, ch2);
+  V P1 = lv_mul(q1, q1), P2 = lv_mul(q2, q2);
+  V mm1 = lv_mul(m1, lv_map(m1, [](float x) { return fabsf(x); }));
+  V mm2 = lv_mul(m2, lv_map(m2, [](float x) { return fabsf(x); }));
+  auto pos_sqrt_f = [](float x) { return fast_sqrt(x > 0.f ? x : 0.f); };
+  V E1 = lv_map(lv_fma(q1, q1, mm1), pos_sqrt_f), E2 = lv_map(lv_fma(q2, q2, mm2), pos_sqrt_f);
+  auto tclamp = [](float mm, float P) { return fmaxf(mm, -P); };  // E^2 - |p|^2 after the R2 clamp
+  V t = lv_add(lv_map2(mm1, P1, tclamp), lv_map2(mm2, P2, tclamp));
+  V inner = lv_fma(sh1, sh2, c);
+  V y = lv_mul(lv_mul(pt1, pt2), inner);
+  V x = lv_fma(E1, E2, lv_mul(y, MONE));
+  V m2sq = lv_fma(x, TWO, t);
+  return lv_map(m2sq, [](float v) { return v >= 0.f ? fast_sqrt(v) : -fast_sqrt(-v); });
 }
 
 // vec_out (WANT_VEC): the boosted pair in the rotated frame, (a2x, a2y, a2z, a2t, b2x, b2y, b2z, b2t).
