@@ -952,3 +952,41 @@ print("OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, PYTHONPATH=root))
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_bench_step_histograms_full_size(gvx, O, dt):
+    """The bench step's two histogram kernels at its size (1e8 pairs, default launch: the
+    two-event TMA rings): sampled masses vs the oracle (lab and CM), bins == FindBin of the
+    kernel's own masses over all 1e8 events, and 4-shard accumulation bit-equal."""
+    import synth.device as sd
+    n = 100_000_000
+    v1, v2 = sd.muon_pairs(n, dtype=TDT[dt])
+    idx = _sample_idx(n, seed=13)
+    a, b = synth.muon_pairs(idx, dtype=dt)
+    sel = torch.from_numpy(idx).cuda()
+    tau = tau_of(dt)
+    for cm in (False, True):
+        m_out = torch.empty(n, dtype=TDT[dt], device="cuda")
+        h = gvx.mass_histogram(v1, v2, cm=cm, m_out=m_out)
+        assert int(h.sum()) == n
+        x = m_out.double()
+        q = (float(NB) * (x - LO)) / (HI - LO)
+        inner = 1 + torch.trunc(torch.nan_to_num(q, nan=0.0, posinf=0.0, neginf=0.0)).long()
+        bb = torch.where(x < LO, 0, torch.where(~(x < HI), NB + 1, inner))
+        assert torch.equal(torch.bincount(bb, minlength=NB + 2), h), cm
+        del x, q, inner, bb
+        acc = gvx.new_bins()
+        for r in range(4):
+            lo_, hi_ = synth.shard_range(n, r, 4)
+            gvx.mass_histogram(v1[lo_:hi_], v2[lo_:hi_], cm=cm, bins=acc)
+        assert torch.equal(acc, h), cm
+        mo, e = (O.cm_mass(a, b) if cm else O.invariant_mass(a, b))
+        mlab, _ = O.invariant_mass(a, b)
+        mg = host(m_out[sel])
+        if cm:
+            ok = np.isfinite(mo) & (np.abs(mlab.astype(np.float64)) >= (1e-2 if dt == np.float32 else 1e-6) * e)
+        else:
+            ok = np.ones(idx.size, bool)
+        assert mass_violations(mg[ok], mo[ok], e[ok], tau).size == 0, cm
+        del m_out
