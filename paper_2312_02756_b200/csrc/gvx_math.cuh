@@ -477,7 +477,8 @@ __device__ __forceinline__ float cos_polar(const V4<float>& v) {
 template <typename T, bool A_Y0 = false, bool WANT_COS = false>
 __device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>* a_out, V4<T>* b_out,
                                           T* cos_out = nullptr) {
-  T Px = a.x + b.x, Py = a.y + b.y, Pz = a.z + b.z, E = a.t + b.t;
+  // A_Y0: a.y is exactly zero, so P_y = b.y (0 + b.y differs at most in the sign of a zero)
+  T Px = a.x + b.x, Py = A_Y0 ? b.y : a.y + b.y, Pz = a.z + b.z, E = a.t + b.t;
   T inv = any_rcp(E);
   BoostCoef<T> k = boost_coef_fast(-Px * inv, -Py * inv, -Pz * inv);
   const bool ok = k.ok && is_positive(E);
