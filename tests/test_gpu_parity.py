@@ -990,3 +990,36 @@ def test_bench_step_histograms_full_size(gvx, O, dt):
             ok = np.ones(idx.size, bool)
         assert mass_violations(mg[ok], mo[ok], e[ok], tau).size == 0, cm
         del m_out
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_fast_domain_edges(gvx, O, dt):
+    """Inputs just inside (and just outside) the fast-path domain of the GPU arithmetic
+    (|eta| < 20, |phi| < 1024 f64 / 8 f32, 2^-200 (f64) / 2^-40 (f32) <= pt, pt and |m| large):
+    lab mass, CM mass and cos theta* within the north-star tolerance of the oracle."""
+    rng = np.random.default_rng(23)
+    n = 20_000
+    phimax = 1023.9 if dt == np.float64 else 7.99
+    ptmin = 2.0 ** -199 if dt == np.float64 else 2.0 ** -39
+
+    def vecs():
+        v = np.empty((n, 4))
+        v[:, 0] = np.exp(rng.uniform(np.log(1e-3), np.log(1e4), n))
+        v[:, 1] = rng.choice([-1, 1], n) * rng.uniform(15.0, 20.5, n)       # some beyond 20: cold path
+        v[:, 2] = rng.choice([-1, 1], n) * rng.uniform(0.9, 1.02, n) * phimax
+        v[:, 3] = rng.uniform(-5.0, 100.0, n)
+        v[: n // 20, 0] = ptmin * rng.uniform(0.5, 4.0, n // 20)          # around the pt lower bound
+        return v.astype(dt)
+
+    v1, v2 = vecs(), vecs()
+    tau = tau_of(dt)
+    e = energy_scale(O, v1, v2)
+    mo, _ = O.invariant_mass(v1, v2)
+    m = host(gvx.invariant_mass(dev(v1), dev(v2)))
+    assert mass_violations(m, mo, e, tau).size == 0
+    mcm, _ = O.cm_mass(v1, v2)
+    m_out = torch.empty(n, dtype=TDT[dt], device="cuda")
+    gvx.mass_histogram(dev(v1), dev(v2), cm=True, m_out=m_out)
+    mlab = mo.astype(np.float64)
+    ok = np.isfinite(mcm) & (np.abs(mlab) >= (1e-2 if dt == np.float32 else 1e-6) * e)
+    assert mass_violations(host(m_out)[ok], mcm[ok], e[ok], tau).size == 0
