@@ -216,6 +216,8 @@ gvx_status gvx_cm_costheta_histogram(gvx_dtype dtype, gvx_coords coords, const g
  *   m_out     NULL or n_events masses of dtype: the pair mass, NaN if the event
  *             is not selected.
  * The number of selected events is the sum of the bins this call added.
+ * Limit: nbins + 2 <= 49152 (the counters are privatised in shared memory);
+ * larger axes -> GVX_ERR_UNSUPPORTED, nothing enqueued.
  */
 gvx_status gvx_dimuon_histogram(gvx_dtype dtype, const gvx_vec4_cview *muons, const int32_t *charge,
                                 const int64_t *offsets, int64_t n_events, double lo, double hi,

@@ -1023,3 +1023,16 @@ def test_fast_domain_edges(gvx, O, dt):
     mlab = mo.astype(np.float64)
     ok = np.isfinite(mcm) & (np.abs(mlab) >= (1e-2 if dt == np.float32 else 1e-6) * e)
     assert mass_violations(host(m_out)[ok], mcm[ok], e[ok], tau).size == 0
+
+
+def test_cm_costheta_large_axes(gvx, O):
+    """Axes too large for shared-memory privatisation take the global-atomics kernel; counts
+    still match the oracle's histograms (well-separated bins: no edge ambiguity at 1e-3 width)."""
+    v1, v2 = synth.muon_pairs(np.arange(30_000), seed=41, dtype=np.float64)
+    mb, cb = gvx.cm_costheta_histogram(dev(v1), dev(v2), m_axis=(0.0, 300.0, 60_000), c_axis=(-1.0, 1.0, 2_000))
+    mbo, cbo, mo, co = O.cm_costheta(v1, v2, m_axis=(0.0, 300.0, 60_000), c_axis=(-1.0, 1.0, 2_000))
+    _, _, _, _, delta, nanp, mlab, e = _costheta_reference(O, v1, v2, np.float64)
+    fails, _ = hist_check_delta(host(cb), co, delta, -1.0, 1.0, 2_000, nan_possible=nanp)
+    assert not fails, fails
+    fails, _ = hist_check(host(mb), mo, e, 1e-12, 0.0, 300.0, 60_000, nan_possible=nanp, m_window_center=mlab)
+    assert not fails, fails
