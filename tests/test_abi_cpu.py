@@ -119,6 +119,18 @@ def test_mass_histogram_peers_validation(gvx):
     assert P(gvx.GVX_F64, 0, by(a), by(b), 0, 0.0, 1.0, 10, 0x4000, 2, None, 0, None, None) == 0   # n == 0
 
 
+def test_dimuon_axis_limit(gvx):
+    """gvx_dimuon_histogram privatises its counters in shared memory: nbins + 2 > 49152 is
+    GVX_ERR_UNSUPPORTED (documented in gvx.h), returned before anything is launched."""
+    L = gvx.lib
+    mu = _view()
+    r = L.gvx_dimuon_histogram(gvx.GVX_F64, ctypes.byref(mu), 0x5000, 0x6000, 10, 0.0, 1.0, 60_000, 0x7000, None,
+                               None)
+    assert r == 3
+    assert L.gvx_dimuon_histogram(gvx.GVX_F64, ctypes.byref(mu), 0x5000, 0x6000, 10, 1.0, 1.0, 10, 0x7000, None,
+                                  None) == 1
+
+
 def test_lorentz_matrix_validation(gvx):
     """gvx_lorentz_transform checks L^T g L = g on the host before anything is enqueued."""
     L = gvx.lib
