@@ -318,8 +318,12 @@ gvx_status dispatch_mass(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, voi
   int L = (l1 == l2) ? l1 : L_GEN;
   if (L == L_AOS && !aligned(m, Group<T, L_AOS>::G * sizeof(T))) L = L_GEN;  // vector stores
   if (L == L_SOA && !aligned(m, Group<T, L_SOA>::G * sizeof(T))) L = L_GEN;
+  // Below ~1e6 pairs a ring with a handful of tiles per CTA cannot overlap its copies with its
+  // arithmetic; the register kernel's many small CTAs are faster there (f64 AoS: 6.8 vs 8.9 us at
+  // 1e4, 11.1 vs 13.3 us at 3e5; equal at 1e6; the ring wins from 3e6 — CFG2 sweep).
+  const bool small = n < (int64_t(1) << 20) && !getenv("GVX_FORCE_TMA");
   if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
-    if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, PM_MASS>()) {
+    if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, PM_MASS>() && !small) {
       HistParams hp{};
       gvx_status st = launch_pair_tma<T, C, PM_MASS>(v1, v2, n, m, hp, nullptr, nullptr, s);
       if (st != GVX_ERR_UNSUPPORTED) return st;
