@@ -429,8 +429,12 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
       return launch_hist<T, C, L_GEN, CM, true>(v1, v2, n, hp, bins, m_out, bo, s);
     }
   }
+  // Small batches: the register kernels win below ~2.6e5 pairs (1e6 for the f64 CM histogram),
+  // measured with L2 flushed (tools/small_n_probe.py, profiles/r01/small_n_probe.jsonl).
+  const int64_t small_n = (CM && sizeof(T) == 8) ? (int64_t(1) << 20) : (int64_t(1) << 18);
+  const bool small = n < small_n && !getenv("GVX_FORCE_TMA");
   if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
-    if (((l1 == L_AOS && l2 == L_AOS) || (l1 == L_SOA && l2 == L_SOA)) && tma_enabled() &&
+    if (((l1 == L_AOS && l2 == L_AOS) || (l1 == L_SOA && l2 == L_SOA)) && tma_enabled() && !small &&
         tma_preferred<T, CM ? PM_HIST_CM : PM_HIST>()) {
       gvx_status st = launch_pair_tma<T, C, CM ? PM_HIST_CM : PM_HIST>(v1, v2, n, m_out, hp, bins, nullptr, s);
       if (st != GVX_ERR_UNSUPPORTED) return st;
