@@ -162,13 +162,16 @@ bool tma_enabled() {
 // (profiles/r01/sweep_f32_variants.jsonl); the fp32 mass kernel runs faster
 // from registers (LDG.256). GVX_FORCE_TMA=1 routes every AoS pair kernel
 // through the ring (tested).
-template <typename T, int MODE>
-bool tma_preferred() {
+bool force_tma() {
   static const bool force = [] {
     const char* e = getenv("GVX_FORCE_TMA");
     return e && e[0] == '1';
   }();
-  return force || sizeof(T) == 8 || MODE != PM_MASS;
+  return force;
+}
+template <typename T, int MODE>
+bool tma_preferred() {
+  return force_tma() || sizeof(T) == 8 || MODE != PM_MASS;
 }
 
 // ------------------------------------------------------- TMA pair stream ----
@@ -321,7 +324,7 @@ gvx_status dispatch_mass(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, voi
   // Below ~1e6 pairs a ring with a handful of tiles per CTA cannot overlap its copies with its
   // arithmetic; the register kernel's many small CTAs are faster there (f64 AoS: 6.8 vs 8.9 us at
   // 1e4, 11.1 vs 13.3 us at 3e5; equal at 1e6; the ring wins from 3e6 — CFG2 sweep).
-  const bool small = n < (int64_t(1) << 20) && !getenv("GVX_FORCE_TMA");
+  const bool small = n < (int64_t(1) << 20) && !force_tma();
   if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
     if (l1 == L_AOS && l2 == L_AOS && tma_enabled() && tma_preferred<T, PM_MASS>() && !small) {
       HistParams hp{};
@@ -432,7 +435,7 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
   // Small batches: the register kernels win below ~2.6e5 pairs (1e6 for the f64 CM histogram),
   // measured with L2 flushed (tools/small_n_probe.py, profiles/r01/small_n_probe.jsonl).
   const int64_t small_n = (CM && sizeof(T) == 8) ? (int64_t(1) << 20) : (int64_t(1) << 18);
-  const bool small = n < small_n && !getenv("GVX_FORCE_TMA");
+  const bool small = n < small_n && !force_tma();
   if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
     if (((l1 == L_AOS && l2 == L_AOS) || (l1 == L_SOA && l2 == L_SOA)) && tma_enabled() && !small &&
         tma_preferred<T, CM ? PM_HIST_CM : PM_HIST>()) {
