@@ -45,7 +45,7 @@ class HostPipeline:
     """Reusable transfer-inclusive runner for batches of ``n`` events."""
 
     def __init__(self, n: int, dtype: torch.dtype, device, nbins: int = DEFAULT_NBINS, lo: float = DEFAULT_LO,
-                 hi: float = DEFAULT_HI, chunk: int = 1 << 23, coords: str = "ptetaphim"):
+                 hi: float = DEFAULT_HI, chunk: int = 1 << 21, coords: str = "ptetaphim"):
         self.n, self.dtype, self.dev = n, dtype, torch.device(device)
         self.nbins, self.lo, self.hi, self.coords = nbins, lo, hi, coords
         self.chunk = max(1, min(chunk, max(n, 1)))
