@@ -483,6 +483,11 @@ def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
     rest[:, 3] = 45.5
     rest2 = rest.clone()  # a distinct array: both vectors of a pair stream from HBM
     cases["hist_single_bin_stress"] = (lambda: gvx.mass_histogram(rest, rest2, coords="pxpypze"), 8 * es)
+    # resonance admixture: 10 % Z-like pairs, a peaked histogram
+    import synth.device as sd
+    z1, z2 = sd.muon_pairs(n, dtype=v1.dtype, device=v1.device, f_res=0.1)
+    cases["hist_fres0.1"] = (lambda: gvx.mass_histogram(z1, z2), 8 * es)
+    cases["hist_cm_fres0.1"] = (lambda: gvx.mass_histogram(z1, z2, cm=True), 8 * es)
     # jagged events (f4): 1 event per pair slot of the batch, ~1.1 muons/event on average
     import synth.device as sd
     jmu, jq, joff = sd.jagged_events(0, n, dtype=v1.dtype, device=v1.device)
@@ -504,7 +509,7 @@ def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
     out["dimuon_jagged"]["note"] = ("bytes/event = offsets + charges of 2-muon events + kinematics of "
                                     "selected events (algorithmic)")
     out["hist_single_bin_stress"]["note"] = "all pairs in one bin (PxPyPzE at rest, M = 91 GeV): atomic contention"
-    del s1, s2, jmu, jq, joff, rest, rest2
+    del s1, s2, jmu, jq, joff, rest, rest2, z1, z2
     return out
 
 

@@ -28,6 +28,8 @@ the muon mass"):
 * per-event beta: isotropic direction g/|g| (g_i Irwin–Hall normals) times
   |β| = 0.99·max(u_a, u_b, u_c) — the max of three uniforms has density
   3r², i.e. β uniform in the ball of radius 0.99.
+* optional resonance admixture (``muon_pairs(..., f_res)``): a
+  fraction f_res of the pairs peaks at the Z mass (see muon_pairs).
 """
 from __future__ import annotations
 
@@ -48,6 +50,9 @@ STREAM_BOOST_P = 3
 STREAM_BOOST_BETA = 4
 STREAM_JAGGED_N = 5     # per-event muon multiplicity
 STREAM_JAGGED_MU = 6    # muon j of event e: counter e * 8 + j (j < 8)
+STREAM_RES = 7          # resonance admixture: selector, then two normals
+Z_MASS = 91.1876
+Z_HALF_WIDTH = 1.2476   # Gamma_Z / 2
 JAGGED_SLOTS = 8
 # multiplicity k = 0..4 with P = 0.25, 0.30, 0.30, 0.10, 0.05 (cumulative thresholds)
 JAGGED_CDF = (0.25, 0.55, 0.85, 0.95)
@@ -125,6 +130,10 @@ def _exp_det(x):
 
 def muons(idx, stream, seed=DEFAULT_SEED, dtype=np.float64):
     """PtEtaPhiM muons for the given global event indices -> [len(idx), 4] of dtype."""
+    return _muons64(idx, stream, seed).astype(dtype)
+
+
+def _muons64(idx, stream, seed=DEFAULT_SEED):
     idx = np.asarray(idx, np.uint64).reshape(-1)
     w0 = _draw(idx, 0, stream, seed)
     w1 = _draw(idx, 1, stream, seed)
@@ -136,12 +145,35 @@ def muons(idx, stream, seed=DEFAULT_SEED, dtype=np.float64):
     out[:, 1] = eta
     out[:, 2] = phi
     out[:, 3] = MUON_MASS
-    return out.astype(dtype)
+    return out
 
 
-def muon_pairs(idx, seed=DEFAULT_SEED, dtype=np.float64):
-    """(v1, v2): two independent PtEtaPhiM muons per event index."""
-    return muons(idx, STREAM_V1, seed, dtype), muons(idx, STREAM_V2, seed, dtype)
+def muon_pairs(idx, seed=DEFAULT_SEED, dtype=np.float64, f_res=0.0):
+    """(v1, v2): two independent PtEtaPhiM muons per event index; with ``f_res`` > 0 that
+    fraction of the events is re-drawn as a resonance pair (SURVEY §8(d) "resonance
+    admixture"): a Z-like mass x = 91.1876 + 1.2476·z1/z2 (ratio of normals: a Breit–Wigner
+    shape; outside [60, 120] GeV it falls back to 91.1876 + 1.2476·z1), muon 2 put back to back
+    in φ with the pt that gives a massless pair this mass, pt2 = x² / (2·pt1·(cosh Δη + 1)).
+    Choosing pt2 inverts the massless back-to-back relation; no 4-vector arithmetic of the
+    method (conversion, sum, mass, boost) is done here."""
+    idx = np.asarray(idx, np.uint64).reshape(-1)
+    a = _muons64(idx, STREAM_V1, seed)
+    b = _muons64(idx, STREAM_V2, seed)
+    if f_res > 0.0:
+        sel = _u(_draw(idx, 0, STREAM_RES, seed)[0]) < f_res
+        if sel.any():
+            ii = idx[sel]
+            z1 = _normal(_draw(ii, 1, STREAM_RES, seed))
+            z2 = _normal(_draw(ii, 2, STREAM_RES, seed))
+            with np.errstate(divide="ignore", invalid="ignore"):
+                x = Z_MASS + Z_HALF_WIDTH * (z1 / z2)
+            x = np.where((x >= 60.0) & (x <= 120.0), x, Z_MASS + Z_HALF_WIDTH * z1)
+            d = a[sel, 1] - b[sel, 1]
+            ch = (_exp_det(d) + _exp_det(-d)) * 0.5
+            b[sel, 0] = (x * x) / ((2.0 * a[sel, 0]) * (ch + 1.0))
+            phi2 = a[sel, 2] + PI
+            b[sel, 2] = np.where(phi2 >= PI, phi2 - TWO_PI, phi2)
+    return a.astype(dtype), b.astype(dtype)
 
 
 def boost_inputs(idx, seed=DEFAULT_SEED, dtype=np.float64):

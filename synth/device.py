@@ -24,6 +24,7 @@ def _load():
             f.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
                           ctypes.c_void_p, ctypes.c_void_p]
             f.restype = ctypes.c_int
+        lib.gvx_synth_muon_pairs.argtypes = lib.gvx_synth_muon_pairs.argtypes + [ctypes.c_double]
         lib.gvx_synth_jagged_counts.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
                                                 ctypes.c_void_p]
         lib.gvx_synth_jagged_counts.restype = ctypes.c_int
@@ -40,8 +41,10 @@ def _code(dtype):
     return 1 if dtype == torch.float64 else 0
 
 
-def muon_pairs(n: int, first: int = 0, seed: int = DEFAULT_SEED, dtype=torch.float64, device="cuda", out=None):
-    """(v1, v2) [n, 4] PtEtaPhiM AoS for global event indices first .. first+n-1."""
+def muon_pairs(n: int, first: int = 0, seed: int = DEFAULT_SEED, dtype=torch.float64, device="cuda", out=None,
+               f_res: float = 0.0):
+    """(v1, v2) [n, 4] PtEtaPhiM AoS for global event indices first .. first+n-1 (``f_res``: the
+    fraction of Z-like resonance pairs, see synth.muon_pairs)."""
     dev = torch.device(device)
     if out is None:
         v1 = torch.empty((n, 4), dtype=dtype, device=dev)
@@ -50,7 +53,7 @@ def muon_pairs(n: int, first: int = 0, seed: int = DEFAULT_SEED, dtype=torch.flo
         v1, v2 = out
     with torch.cuda.device(dev):
         rc = _load().gvx_synth_muon_pairs(_code(dtype), seed, first, n, v1.data_ptr(), v2.data_ptr(),
-                                          torch.cuda.current_stream(dev).cuda_stream)
+                                          torch.cuda.current_stream(dev).cuda_stream, float(f_res))
     if rc:
         raise RuntimeError(f"gvx_synth_muon_pairs: cuda error {rc}")
     return v1, v2

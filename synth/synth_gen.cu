@@ -12,7 +12,7 @@ namespace {
 
 constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
 constexpr uint32_t STREAM_V1 = 1, STREAM_V2 = 2, STREAM_BOOST_P = 3, STREAM_BOOST_BETA = 4;
-constexpr uint32_t STREAM_JAGGED_N = 5, STREAM_JAGGED_MU = 6, JAGGED_SLOTS = 8;
+constexpr uint32_t STREAM_JAGGED_N = 5, STREAM_JAGGED_MU = 6, JAGGED_SLOTS = 8, STREAM_RES = 7;
 
 __device__ __forceinline__ uint4 philox(uint64_t idx, uint32_t call, uint32_t stream, uint64_t seed) {
   uint32_t c0 = (uint32_t)idx, c1 = (uint32_t)(idx >> 32), c2 = call, c3 = stream;
@@ -50,26 +50,48 @@ __device__ __forceinline__ double exp_det(double x) {
   return scalbn(p, (int)k);
 }
 
+__device__ __forceinline__ void muon64(uint64_t idx, uint32_t stream, uint64_t seed, double (&o)[4]) {
+  uint4 w0 = philox(idx, 0, stream, seed), w1 = philox(idx, 1, stream, seed);
+  o[0] = exp_det(__dadd_rn(3.4011973816621555, __dmul_rn(0.5, normal4(w0))));
+  o[1] = __dadd_rn(-2.5, __dmul_rn(5.0, u01(w1.x)));
+  o[2] = __dadd_rn(-3.141592653589793, __dmul_rn(6.283185307179586, u01(w1.y)));
+  o[3] = 0.1056583755;
+}
 template <typename T>
 __device__ __forceinline__ void muon(uint64_t idx, uint32_t stream, uint64_t seed, T* out) {
-  uint4 w0 = philox(idx, 0, stream, seed), w1 = philox(idx, 1, stream, seed);
-  double pt = exp_det(__dadd_rn(3.4011973816621555, __dmul_rn(0.5, normal4(w0))));
-  double eta = __dadd_rn(-2.5, __dmul_rn(5.0, u01(w1.x)));
-  double phi = __dadd_rn(-3.141592653589793, __dmul_rn(6.283185307179586, u01(w1.y)));
-  out[0] = (T)pt;
-  out[1] = (T)eta;
-  out[2] = (T)phi;
-  out[3] = (T)0.1056583755;
+  double o[4];
+  muon64(idx, stream, seed, o);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k] = (T)o[k];
+}
+
+// Resonance admixture (see synth/__init__.py, resonance_pairs): with probability
+// f_res the pair is re-drawn as a Z-like peak: muon 2 is put back to back in phi
+// with pt chosen for a massless pair mass x (ratio-of-normals Breit-Wigner shape
+// around 91.1876 GeV, half width 1.2476, kept in [60, 120]).
+__device__ __forceinline__ void resonance(uint64_t idx, uint64_t seed, double f_res, const double (&a)[4],
+                                          double (&b)[4]) {
+  if (!(u01(philox(idx, 0, STREAM_RES, seed).x) < f_res)) return;
+  const double z1 = normal4(philox(idx, 1, STREAM_RES, seed)), z2 = normal4(philox(idx, 2, STREAM_RES, seed));
+  double x = __dadd_rn(91.1876, __dmul_rn(1.2476, __ddiv_rn(z1, z2)));
+  if (!(x >= 60.0 && x <= 120.0)) x = __dadd_rn(91.1876, __dmul_rn(1.2476, z1));
+  const double d = __dsub_rn(a[1], b[1]);
+  const double ch = __dmul_rn(__dadd_rn(exp_det(d), exp_det(-d)), 0.5);
+  b[0] = __ddiv_rn(__dmul_rn(x, x), __dmul_rn(__dmul_rn(2.0, a[0]), __dadd_rn(ch, 1.0)));
+  const double phi2 = __dadd_rn(a[2], 3.141592653589793);
+  b[2] = phi2 >= 3.141592653589793 ? __dsub_rn(phi2, 6.283185307179586) : phi2;
 }
 
 template <typename T>
-__global__ void k_muon_pairs(uint64_t seed, uint64_t first, int64_t n, T* v1, T* v2) {
+__global__ void k_muon_pairs(uint64_t seed, uint64_t first, int64_t n, T* v1, T* v2, double f_res) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    T a[4], b[4];
-    muon<T>(first + (uint64_t)i, STREAM_V1, seed, a);
-    muon<T>(first + (uint64_t)i, STREAM_V2, seed, b);
+    double a[4], b[4];
+    const uint64_t idx = first + (uint64_t)i;
+    muon64(idx, STREAM_V1, seed, a);
+    muon64(idx, STREAM_V2, seed, b);
+    if (f_res > 0.0) resonance(idx, seed, f_res, a, b);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) { v1[4 * i + k] = a[k]; v2[4 * i + k] = b[k]; }
+    for (int k = 0; k < 4; ++k) { v1[4 * i + k] = (T)a[k]; v2[4 * i + k] = (T)b[k]; }
   }
 }
 
@@ -199,11 +221,13 @@ extern "C" {
 
 // dtype: 0 = float32, 1 = float64. v1, v2: AoS [n][4] device buffers; v: [n][4],
 // beta: [n][3]. Returns 0 or a cudaError_t value.
-int gvx_synth_muon_pairs(int dtype, uint64_t seed, uint64_t first, int64_t n, void* v1, void* v2, void* stream) {
+// f_res: fraction of resonance (Z-like) pairs, 0 for independent muons.
+int gvx_synth_muon_pairs(int dtype, uint64_t seed, uint64_t first, int64_t n, void* v1, void* v2, void* stream,
+                         double f_res) {
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == 1) k_muon_pairs<double><<<grid_of(n), 256, 0, s>>>(seed, first, n, (double*)v1, (double*)v2);
-  else k_muon_pairs<float><<<grid_of(n), 256, 0, s>>>(seed, first, n, (float*)v1, (float*)v2);
+  if (dtype == 1) k_muon_pairs<double><<<grid_of(n), 256, 0, s>>>(seed, first, n, (double*)v1, (double*)v2, f_res);
+  else k_muon_pairs<float><<<grid_of(n), 256, 0, s>>>(seed, first, n, (float*)v1, (float*)v2, f_res);
   return (int)cudaGetLastError();
 }
 

@@ -87,6 +87,9 @@ def test_synth_device_matches_host(dt, first):
     v1d, v2d = sd.muon_pairs(n, first=first, dtype=TDT[dt])
     v1h, v2h = synth.muon_pairs(np.arange(first, first + n), dtype=dt)
     assert np.array_equal(host(v1d), v1h) and np.array_equal(host(v2d), v2h)
+    r1d, r2d = sd.muon_pairs(n, first=first, dtype=TDT[dt], f_res=0.1)  # resonance admixture twin
+    r1h, r2h = synth.muon_pairs(np.arange(first, first + n), dtype=dt, f_res=0.1)
+    assert np.array_equal(host(r1d), r1h) and np.array_equal(host(r2d), r2h)
     vd, bd = sd.boost_inputs(n, first=first, dtype=TDT[dt])
     vh, bh = synth.boost_inputs(np.arange(first, first + n), dtype=dt)
     assert np.array_equal(host(vd), vh) and np.array_equal(host(bd), bh)

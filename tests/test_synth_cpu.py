@@ -50,3 +50,25 @@ def test_distribution_recipe():
 def test_exp_det_accuracy():
     x = np.linspace(-30, 30, 200001)
     assert np.max(np.abs(synth._exp_det(x) / np.exp(x) - 1)) < 1e-15
+
+
+def test_resonance_admixture():
+    """f_res: that fraction of pairs is re-drawn as a Z-like peak (muon 2 back to back in phi,
+    pt chosen for a massless pair of mass x in [60, 120]); f_res = 0 leaves the batch
+    unchanged; muon 1 is never touched; the resonance masses (evaluated here along the
+    rapidity-angle form, independent of the oracle) peak at 91.19 GeV."""
+    idx = np.arange(200_000)
+    a0, b0 = synth.muon_pairs(idx)
+    a, b = synth.muon_pairs(idx, f_res=0.1)
+    assert np.array_equal(a, a0)
+    res = ~np.all(b == b0, axis=1)
+    assert abs(res.mean() - 0.1) < 0.005
+    dphi = np.abs(a[res, 2] - b[res, 2])
+    assert np.allclose(dphi, np.pi, atol=1e-12)
+    pt1, eta1, pt2, eta2 = a[res, 0], a[res, 1], b[res, 0], b[res, 1]
+    m2 = 2 * pt1 * pt2 * (np.cosh(eta1 - eta2) + 1)  # massless, back to back in phi
+    m = np.sqrt(m2)
+    assert np.all((m > 59.9) & (m < 120.1))
+    assert abs(np.median(m) - 91.19) < 0.2
+    a1, b1 = synth.muon_pairs(idx, f_res=0.0)
+    assert np.array_equal(b1, b0)
