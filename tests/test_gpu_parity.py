@@ -1039,3 +1039,16 @@ def test_cm_costheta_large_axes(gvx, O):
     assert not fails, fails
     fails, _ = hist_check(host(mb), mo, e, 1e-12, 0.0, 300.0, 60_000, nan_possible=nanp, m_window_center=mlab)
     assert not fails, fails
+
+
+def test_boost_high_beta_f64(gvx, O):
+    """fp64 boosts at |β| = 0.999 … 0.9999 (reading R10's stress set) within τ·S of the oracle."""
+    rng = np.random.default_rng(78)
+    n = 100_000
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    beta = d * rng.uniform(0.999, 0.9999, size=(n, 1))
+    v, _ = synth.boost_inputs(np.arange(n), seed=4)
+    ref, S = O.boost(v, beta)
+    out = host(gvx.boost(dev(v), dev(beta)))
+    assert boost_violations(out, ref, S, 1e-12).size == 0

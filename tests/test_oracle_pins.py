@@ -654,3 +654,21 @@ def test_costheta_degenerate_and_histograms(O):
     assert cb[1:26].sum() > 1000 and cb[26:51].sum() > 1000
     mb2, cb2, _, _ = O.cm_costheta(v1, v2, c_axis=(-1.0, 1.0, 50), m_bins=mb.copy(), c_bins=cb.copy())
     assert np.array_equal(cb2, 2 * cb) and np.array_equal(mb2, 2 * mb)
+
+
+def test_boost_high_beta_stress(O):
+    """Reading R10's fp64 stress set: |β| up to 0.9999 (γ ≈ 71). The literal Λ stays within
+    τ·S of the rapidity-route truth (the rounding of 1 − β² grows as 1/(1 − β²))."""
+    rng = np.random.default_rng(77)
+    n = 300
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    mag = np.concatenate([np.full(n // 3, 0.999), np.full(n // 3, 0.9995), np.full(n - 2 * (n // 3), 0.9999)])
+    beta = d * mag[:, None]
+    v, _ = synth.boost_inputs(np.arange(n), seed=3)
+    out, S = O.boost(v, beta)
+    worst = 0.0
+    for i in range(n):
+        t = truth_boost(v[i], beta[i])
+        worst = max(worst, max(abs(float(out[i, k]) - float(t[k])) for k in range(4)) / float(S[i]))
+    assert worst <= 1e-12, worst
