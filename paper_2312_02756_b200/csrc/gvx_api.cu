@@ -279,6 +279,8 @@ gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, i
       case 4: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 768, 4, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       case 5: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 512, 4, 16, 2>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       case 6: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1536, 4, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 7: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1280, 5, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 8: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1024, 6, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       default: break;
     }
   }
