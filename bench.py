@@ -36,8 +36,12 @@ BYTES = {
     "boost": lambda es: 4 * es + 3 * es + 4 * es,  # vector + beta in, vector out
     "mass_histogram": lambda es: 8 * es,           # two vectors in (bins: per-call constant)
     "mass_histogram_cm": lambda es: 8 * es,
+    "pairs": lambda es: 8 * es + es,               # fused pass: pairs in once, lab masses out
 }
 KERNEL_ORDER = ["invariant_mass", "boost", "mass_histogram", "mass_histogram_cm"]
+# The default step: gvx_pair_histograms (lab mass + lab histogram + CM mass + CM histogram in ONE
+# pass over the pairs, bit-identical to the three separate kernels) and the boost.
+FUSED_ORDER = ["pairs", "boost"]
 # Λ(β = (0, 0, 0.6)) · R_z(0.7): a general Lorentz transformation for the --extended timing
 _c, _s, _g = 0.7648421872844885, 0.644217687237691, 1.25
 LORENTZ_DEMO = [[_c, -_s, 0, 0], [_s, _c, 0, 0], [0, 0, _g, _g * 0.6], [0, 0, _g * 0.6, _g]]
@@ -55,6 +59,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=1 << 22, help="events in the oracle's bounded sample")
     p.add_argument("--dist-backend", default="nccl", help="process-group backend for N>1 (nccl on B200s)")
+    p.add_argument("--unfused", action="store_true",
+                   help="time the step as four kernels (mass, boost, lab histogram, CM histogram) instead of the "
+                        "fused pair pass + boost")
     p.add_argument("--bin-reduce", choices=["nccl", "p2p"], default="nccl",
                    help="N>1 bin reduction: NCCL all-reduce after the kernel, or fused into the kernel tail "
                         "(P2P atomics into every rank's symmetric-memory bins, SURVEY 8(e))")
@@ -222,6 +229,9 @@ def config_obj(args, world, ref_sample=None):
              "bin all-reduce fused into the kernel tail: P2P atomics into symmetric memory)"
              if world > 1 and getattr(args, "bin_reduce", "nccl") == "p2p" and getattr(args, "dist_backend", "nccl") == "nccl"
              else f"{getattr(args, 'dist_backend', 'nccl')} bin all-reduce)")}
+    c["kernels"] = ("four kernels: mass, boost, lab histogram, CM histogram" if getattr(args, "unfused", False)
+                    else "gvx_pair_histograms (lab mass + lab histogram + CM mass + CM histogram in one pass over "
+                         "the pairs, bit-identical to the separate kernels) + boost")
     if ref_sample:
         c["reference_sample_events"] = ref_sample
     return c
@@ -328,14 +338,27 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
 
     p2p = world > 1 and args.bin_reduce == "p2p" and args.dist_backend == "nccl"
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-    kern_ms = {k: [] for k in KERNEL_ORDER}
+    fused = not args.unfused and not p2p
+    order = FUSED_ORDER if fused else KERNEL_ORDER
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(order) + 1)]
+    kern_ms = {k: [] for k in order}
 
     def step(record: bool):
         bins.zero_()
         bins_cm.zero_()
         if record:
             ev[0].record(stream)
+        if fused:
+            gvx.pair_histograms(v1, v2, LO, HI, NB, lab_bins=bins, cm_bins=bins_cm, m_out=m)
+            if record:
+                ev[1].record(stream)
+            gvx.boost(bv, bb, out=bout)
+            if record:
+                ev[2].record(stream)
+            if world > 1:
+                gvx.allreduce_bins(bins)
+                gvx.allreduce_bins(bins_cm)
+            return
         gvx.invariant_mass(v1, v2, out=m)
         if record:
             ev[1].record(stream)
@@ -373,8 +396,8 @@ def run_ours(args):
         t_start.record(stream)
         for _ in range(args.steps):
             step(True)
-            ev[4].synchronize()
-            for i, k in enumerate(KERNEL_ORDER):
+            ev[-1].synchronize()
+            for i, k in enumerate(order):
                 kern_ms[k].append(ev[i].elapsed_time(ev[i + 1]))
         t_end.record(stream)
         torch.cuda.synchronize(dev)
@@ -392,26 +415,30 @@ def run_ours(args):
     # per-kernel breakdown (CUDA events on the launch stream, averaged over the timed steps)
     peak, peak_kind = peaks()
     kernels = {}
-    for k in KERNEL_ORDER:
+    for k in order:
         avg = sum(kern_ms[k]) / len(kern_ms[k])
         bpe = BYTES[k](es)
         gbs = n * bpe / (avg * 1e-3) / 1e9
         kernels[k] = {"ms": avg, "events_per_s": n / (avg * 1e-3), "bytes_per_event": bpe,
                       "achieved_GBs": gbs, "frac_of_peak": gbs / peak}
-    dom = max(KERNEL_ORDER, key=lambda k: kernels[k]["ms"])
-    step_bytes = n * sum(BYTES[k](es) for k in KERNEL_ORDER)
+    dom = max(order, key=lambda k: kernels[k]["ms"])
+    step_bytes = n * sum(BYTES[k](es) for k in order)
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9  # per GPU: each rank moves step_bytes
     roofline = {"bound": "hbm", "kernel": f"gvx_{dom}", "achieved": kernels[dom]["achieved_GBs"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dom]["frac_of_peak"], "traffic": ncu_traffic(dom, args.dtype, n),
                 "peak_source": peak_kind,
                 "bytes_per_launch": n * BYTES[dom](es)}
+    if dom == "pairs":
+        roofline["note"] = ("the fused pass moves 1/3 of the unfused pair bytes; it is bound by arithmetic "
+                            "(f64: FP64 pipe; f32: issue + MUFU), see profiles/r01/ncu_summary_*.md; "
+                            "--unfused times the four separate kernels")
 
     # K5: the read-only streaming peak measured in this run (one launch over an 8 GB scratch
     # buffer, 64x L2, freed afterwards)
     scratch = torch.empty(8 << 30, dtype=torch.uint8, device=dev)
     read_peak = sd.stream_read_gbs([scratch])
     del scratch
-    for k in KERNEL_ORDER:
+    for k in order:
         kernels[k]["frac_of_read_peak"] = kernels[k]["achieved_GBs"] / read_peak
     extended = run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak) if args.extended else None
 
@@ -432,7 +459,7 @@ def run_ours(args):
             "data": "synthetic (synth/: Philox4x32-10 seeded muon pairs + boost inputs, seed 12345)",
             "config": config_obj(args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": 4 * args.steps, "clocks": clk.summary(), "kernels": kernels,
+            "gpu_launches": len(order) * args.steps, "clocks": clk.summary(), "kernels": kernels,
             "peaks": {"copy_GBs": peak, "copy_source": peak_kind, "read_stream_GBs": read_peak,
                       "read_stream_source": "K5 stream-read probe in this run (synth/libgvxsynth.so: TMA bulk-copy "
                                             "ring, 6 x 16 KB stages per SM, over an 8 GB buffer, best of 5)",

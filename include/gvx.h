@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define GVX_ABI_VERSION 4
+#define GVX_ABI_VERSION 5
 
 typedef struct CUstream_st *gvx_stream_t; /* == cudaStream_t */
 
@@ -154,6 +154,24 @@ gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4
                               int32_t nbins, unsigned long long *bins, uint32_t flags,
                               void *m_out, const gvx_vec4_view *boosted_out,
                               gvx_stream_t stream);
+
+/*
+ * gvx_pair_histograms — the pair kernels of one batch fused into ONE pass over
+ * the inputs: for each pair the lab mass (exactly gvx_invariant_mass's value),
+ * its histogram, the CM mass (exactly gvx_mass_histogram's with
+ * GVX_HIST_BOOST_TO_CM) and its histogram, both on the same axis (lo, hi,
+ * nbins; binning as gvx_mass_histogram). The inputs are read once instead of
+ * three times (mass, lab histogram, CM histogram).
+ *   lab_bins, cm_bins  nbins+2 uint64 each (device), ACCUMULATED.
+ *   m_out, cm_m_out    NULL or n masses of dtype (device): lab / CM.
+ * Results are bit-identical to the three separate calls. Errors as
+ * gvx_mass_histogram.
+ */
+gvx_status gvx_pair_histograms(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview *v1,
+                               const gvx_vec4_cview *v2, int64_t n, double lo, double hi,
+                               int32_t nbins, unsigned long long *lab_bins,
+                               unsigned long long *cm_bins, void *m_out, void *cm_m_out,
+                               gvx_stream_t stream);
 
 /*
  * gvx_mass_histogram_peers — gvx_mass_histogram with the cross-GPU bin

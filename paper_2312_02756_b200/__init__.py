@@ -43,7 +43,7 @@ GVX_PXPYPZE = 1
 GVX_PXPYPZM = 2
 GVX_PTETAPHIE = 3
 GVX_HIST_BOOST_TO_CM = 0x1
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 # The default histogram of the north star: 1000 bins over the dimuon range
 # (reading R13).
@@ -100,6 +100,9 @@ def _load_lib():
     lib.gvx_dimuon_histogram.argtypes = [st, ctypes.POINTER(Vec4CView), P, P, I64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_int32, P, P, P]
     lib.gvx_dimuon_histogram.restype = st
+    lib.gvx_pair_histograms.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P, P, P]
+    lib.gvx_pair_histograms.restype = st
     lib.gvx_mass_histogram_peers.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
                                              ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, ctypes.c_int32,
                                              P, ctypes.c_uint32, P, P]
@@ -408,6 +411,30 @@ def sharded_mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: f
     Returns the global histogram on every rank."""
     bins = mass_histogram(v1, v2, lo, hi, nbins, bins=bins, cm=cm, coords=coords)
     return allreduce_bins(bins, group)
+
+
+def pair_histograms(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = DEFAULT_HI,
+                    nbins: int = DEFAULT_NBINS, lab_bins: Optional[torch.Tensor] = None,
+                    cm_bins: Optional[torch.Tensor] = None, m_out: Optional[torch.Tensor] = None,
+                    cm_m_out: Optional[torch.Tensor] = None, coords: str = "ptetaphim"):
+    """gvx_pair_histograms: lab mass + lab histogram + CM mass + CM histogram of the pairs in ONE
+    pass over the inputs (bit-identical to invariant_mass / mass_histogram / mass_histogram(cm=True)).
+    Returns ``(lab_bins, cm_bins)`` ([nbins+2] int64 each, accumulated)."""
+    a, n, dt, dev, _ = _view(v1, 4, "v1")
+    b, n2, dt2, dev2, _ = _view(v2, 4, "v2")
+    if n != n2:
+        raise ValueError(f"length mismatch: v1 has {n} vectors, v2 has {n2}")
+    if dt != dt2 or dev != dev2:
+        raise ValueError("v1 and v2 must share dtype and device")
+    lab_bins = _bins_arg(lab_bins, nbins, dev, "lab_bins")
+    cm_bins = _bins_arg(cm_bins, nbins, dev, "cm_bins")
+    mptr = _out_1d(m_out, n, dt, "m_out")
+    cptr = _out_1d(cm_m_out, n, dt, "cm_m_out")
+    with torch.cuda.device(dev):
+        _check(lib.gvx_pair_histograms(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b), n,
+                                       float(lo), float(hi), int(nbins), lab_bins.data_ptr(), cm_bins.data_ptr(),
+                                       mptr, cptr, _stream(dev)), "gvx_pair_histograms")
+    return lab_bins, cm_bins
 
 
 def mass_histogram_peers(v1: VecArg, v2: VecArg, peer_bins_dev: int, npeers: int, lo: float = DEFAULT_LO,

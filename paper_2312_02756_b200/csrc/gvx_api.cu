@@ -188,9 +188,11 @@ template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 1
 // fp64 lab histogram: 20 warps x 2 interleaved events, 0.904 vs 0.934 ms (same sweep)
 template <> struct TmaCfgOf<double, PM_HIST> { using type = PairTma<double, 1280, 2, 20, 1>; };
 template <> struct TmaCfgOf<double, PM_HIST_CM_COS> { using type = PairTma<double, 1536, 2, 24, 1>; };
+template <> struct TmaCfgOf<double, PM_BOTH> { using type = PairTma<double, 1536, 2, 24, 1>; };
 template <int MODE> struct TmaCfgOf<float, MODE> { using type = PairTma<float, 896, 4, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM> { using type = PairTma<float, 1792, 3, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM_COS> { using type = PairTma<float, 1792, 3, 28, 1>; };
+template <> struct TmaCfgOf<float, PM_BOTH> { using type = PairTma<float, 1792, 3, 28, 1>; };
 
 #ifdef GVX_TUNE
 // Tuning build only (tools/libgvx_tune.so): GVX_TMA_CFG / GVX_LDG_CFG pick
@@ -211,7 +213,8 @@ gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v
   // AoS (paper layout) or SoA with 16-byte aligned component arrays; else not handled here.
   const bool soa = classify(v1, sizeof(T)) == L_SOA && classify(v2, sizeof(T)) == L_SOA;
   if (!soa && !(classify(v1, sizeof(T)) == L_AOS && classify(v2, sizeof(T)) == L_AOS)) return GVX_ERR_UNSUPPORTED;
-  const int nbs = MODE == PM_MASS ? 0 : hp.nbins + 2 + (MODE == PM_HIST_CM_COS ? co.hc.nbins + 2 : 0);
+  const int nbs =
+      MODE == PM_MASS ? 0 : hp.nbins + 2 + ((MODE == PM_HIST_CM_COS || MODE == PM_BOTH) ? co.hc.nbins + 2 : 0);
   const size_t sm = CFG::smem_bytes(nbs);
   if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
   auto k = soa ? k_pair_tma<T, C, MODE, CFG, false, true> : k_pair_tma<T, C, MODE, CFG, false, false>;
@@ -448,6 +451,29 @@ gvx_status dispatch_hist(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
   if (L == L_AOS) return launch_hist<T, C, L_AOS, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
   if (L == L_SOA) return launch_hist<T, C, L_SOA, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
   return launch_hist<T, C, L_GEN, CM>(v1, v2, n, hp, bins, m_out, nullptr, s);
+}
+
+// ----------------------------------------------- fused lab + CM pass -----
+template <typename T, int C>
+gvx_status dispatch_both(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, const HistParams& hp,
+                         unsigned long long* lab_bins, unsigned long long* cm_bins, void* m_out, void* cm_m_out,
+                         cudaStream_t s) {
+  const int l1 = classify(v1, sizeof(T)), l2 = classify(v2, sizeof(T));
+  const bool small = n < (int64_t(1) << 18) && !force_tma();
+  if constexpr (C == C_PTETAPHIM || C == C_PXPYPZE) {
+    if (((l1 == L_AOS && l2 == L_AOS) || (l1 == L_SOA && l2 == L_SOA)) && tma_enabled() && !small) {
+      CosOut<T> co{hp, cm_bins, (T*)cm_m_out};
+      co.hc.peers = nullptr;  // the CM histogram of the fused pass always lands in cm_bins
+      co.hc.npeers = 0;
+      co.hc.mc = nullptr;
+      gvx_status st = launch_pair_tma<T, C, PM_BOTH>(v1, v2, n, m_out, hp, lab_bins, nullptr, s, co);
+      if (st != GVX_ERR_UNSUPPORTED) return st;
+    }
+  }
+  // other layouts / coordinates / small batches: the two histogram passes
+  gvx_status st = dispatch_hist<T, C, false>(v1, v2, n, hp, lab_bins, m_out, nullptr, s);
+  if (st != GVX_OK) return st;
+  return dispatch_hist<T, C, true>(v1, v2, n, hp, cm_bins, cm_m_out, nullptr, s);
 }
 
 // ------------------------------------------------------ cos theta* -------
@@ -736,6 +762,34 @@ gvx_status gvx_boost_uniform(gvx_dtype dtype, const gvx_vec4_cview* v, double bx
   if (!view_ok<4>(v, es) || !out_view_ok(out, es)) return GVX_ERR_INVALID_ARGUMENT;
   if (dtype == GVX_F64) return launch_boost<double, true>(v, nullptr, out, n, bx, by, bz, s);
   return launch_boost<float, true>(v, nullptr, out, n, (float)bx, (float)by, (float)bz, s);
+}
+
+gvx_status gvx_pair_histograms(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,
+                               const gvx_vec4_cview* v2, int64_t n, double lo, double hi, int32_t nbins,
+                               unsigned long long* lab_bins, unsigned long long* cm_bins, void* m_out,
+                               void* cm_m_out, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || !valid_coords(coords) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GVX_OK;
+  const size_t es = dsize(dtype);
+  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !lab_bins || !aligned(lab_bins, 8) || !cm_bins ||
+      !aligned(cm_bins, 8))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if ((m_out && !aligned(m_out, es)) || (cm_m_out && !aligned(cm_m_out, es))) return GVX_ERR_INVALID_ARGUMENT;
+  const HistParams hp = make_hist_params(lo, hi, nbins);
+  cudaStream_t s = (cudaStream_t)stream;
+#define GVX_BOTH_COORDS(T)                                                                                   \
+  switch (coords) {                                                                                         \
+    case GVX_PTETAPHIM: return dispatch_both<T, C_PTETAPHIM>(v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, s); \
+    case GVX_PXPYPZE: return dispatch_both<T, C_PXPYPZE>(v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, s);     \
+    case GVX_PXPYPZM: return dispatch_both<T, C_PXPYPZM>(v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, s);     \
+    default: return dispatch_both<T, C_PTETAPHIE>(v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, s);            \
+  }
+  if (dtype == GVX_F64) {
+    GVX_BOTH_COORDS(double)
+  }
+  GVX_BOTH_COORDS(float)
+#undef GVX_BOTH_COORDS
 }
 
 gvx_status gvx_cm_costheta_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,

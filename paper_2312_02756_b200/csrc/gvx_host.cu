@@ -181,12 +181,18 @@ gvx_status gvx_host_pairs(gvx_host_pipeline* p, gvx_coords coords, const void* h
     cudaStreamWaitEvent(p->s_cmp, p->ev_in[j], 0);
     gvx_vec4_cview v1 = aos_view(d1, es), v2 = aos_view(d2, es);
     gvx_stream_t sc = (gvx_stream_t)p->s_cmp;
-    if (h_m_out && st == GVX_OK) st = gvx_invariant_mass(p->dtype, coords, &v1, &v2, dm, k, sc);
-    if (h_bins && st == GVX_OK)
-      st = gvx_mass_histogram(p->dtype, coords, &v1, &v2, k, lo, hi, nbins, p->d_bins, 0u, nullptr, nullptr, sc);
-    if (h_bins_cm && st == GVX_OK)
-      st = gvx_mass_histogram(p->dtype, coords, &v1, &v2, k, lo, hi, nbins, p->d_bins + nb2, GVX_HIST_BOOST_TO_CM,
-                              nullptr, nullptr, sc);
+    if (h_bins && h_bins_cm) {  // everything requested: the fused one-pass kernel (same bits)
+      if (st == GVX_OK)
+        st = gvx_pair_histograms(p->dtype, coords, &v1, &v2, k, lo, hi, nbins, p->d_bins, p->d_bins + nb2,
+                                 h_m_out ? dm : nullptr, nullptr, sc);
+    } else {
+      if (h_m_out && st == GVX_OK) st = gvx_invariant_mass(p->dtype, coords, &v1, &v2, dm, k, sc);
+      if (h_bins && st == GVX_OK)
+        st = gvx_mass_histogram(p->dtype, coords, &v1, &v2, k, lo, hi, nbins, p->d_bins, 0u, nullptr, nullptr, sc);
+      if (h_bins_cm && st == GVX_OK)
+        st = gvx_mass_histogram(p->dtype, coords, &v1, &v2, k, lo, hi, nbins, p->d_bins + nb2, GVX_HIST_BOOST_TO_CM,
+                                nullptr, nullptr, sc);
+    }
     cudaEventRecord(p->ev_cmp[j], p->s_cmp);
     cudaStreamWaitEvent(p->s_out, p->ev_cmp[j], 0);
     if (h_m_out) cudaMemcpyAsync((char*)h_m_out + a * es, dm, k * es, cudaMemcpyDeviceToHost, p->s_out);

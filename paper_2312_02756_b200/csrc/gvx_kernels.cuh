@@ -760,7 +760,9 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
 // HBM reads for later stages stay in flight while the FP64 pipe works —
 // bytes in flight are set by STAGES x TILE, not by register occupancy.
 // ============================================================================
-enum PairMode { PM_MASS = 0, PM_HIST = 1, PM_HIST_CM = 2, PM_HIST_CM_COS = 3 };
+// PM_BOTH: lab mass + lab histogram + CM mass + CM histogram in one pass over the
+// pairs (gvx_pair_histograms); the CM histogram and masses use the CosOut slot.
+enum PairMode { PM_MASS = 0, PM_HIST = 1, PM_HIST_CM = 2, PM_HIST_CM_COS = 3, PM_BOTH = 4 };
 
 template <typename T, int TILE_, int STAGES_, int NCW_, int MINB_ = 1>
 struct PairTma {
@@ -802,6 +804,23 @@ __device__ __forceinline__ void pair_consume(const T (&a)[4], const T (&b)[4], i
                                              unsigned int* sh_cos, const CosOut<T>& co) {
   if constexpr (MODE == PM_MASS) {
     m_out[i] = event_mass<T, COORDS>(a, b);
+  } else if constexpr (MODE == PM_BOTH) {
+    T ml, mc;
+    if constexpr (sizeof(T) == 8 && COORDS == C_PTETAPHIM) {
+      if (fast_domain(a[0], a[1], a[2], a[3]) && fast_domain(b[0], b[1], b[2], b[3])) {
+        both_masses_fast(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3], ml, mc);
+      } else {
+        ml = event_mass<T, COORDS>(a, b);
+        mc = hist_event_mass<T, COORDS, true, false>(a, b, i, bo);
+      }
+    } else {
+      ml = event_mass<T, COORDS>(a, b);
+      mc = hist_event_mass<T, COORDS, true, false>(a, b, i, bo);
+    }
+    atomicAdd(&sh_hist[find_bin(ml, hp)], 1u);
+    atomicAdd(&sh_cos[find_bin(mc, co.hc)], 1u);
+    if (m_out) m_out[i] = ml;
+    if (co.cos_out) co.cos_out[i] = mc;
   } else if constexpr (MODE == PM_HIST_CM_COS) {
     T c;
     T M = hist_event_mass<T, COORDS, true, WANT_BO, true>(a, b, i, bo, &c);
@@ -832,7 +851,23 @@ __device__ __forceinline__ void pair_consume_x2(const float (&a0)[4], const floa
                  A3 = make_float2(a0[3], a1[3]), B0 = make_float2(b0[0], b1[0]), B1 = make_float2(b0[1], b1[1]),
                  B2 = make_float2(b0[2], b1[2]), B3 = make_float2(b0[3], b1[3]);
     float2 M;
-    if constexpr (MODE == PM_MASS || MODE == PM_HIST) {
+    if constexpr (MODE == PM_BOTH) {
+      M = pair_mass_f32_lanes<float2>(A0, A1, A2, A3, B0, B1, B2, B3);
+      const float2 C = cm_mass_f32_lanes<float2, false, false>(A0, A1, A2, A3, B0, B1, B2, B3, &c, nullptr);
+      atomicAdd(&sh_hist[find_bin(M.x, hp)], 1u);
+      atomicAdd(&sh_hist[find_bin(M.y, hp)], 1u);
+      atomicAdd(&sh_cos[find_bin(C.x, co.hc)], 1u);
+      atomicAdd(&sh_cos[find_bin(C.y, co.hc)], 1u);
+      if (m_out) {
+        m_out[i0] = M.x;
+        m_out[i1] = M.y;
+      }
+      if (co.cos_out) {
+        co.cos_out[i0] = C.x;
+        co.cos_out[i1] = C.y;
+      }
+      return;
+    } else if constexpr (MODE == PM_MASS || MODE == PM_HIST) {
       M = pair_mass_f32_lanes<float2>(A0, A1, A2, A3, B0, B1, B2, B3);
       if constexpr (MODE == PM_MASS) {
         m_out[i0] = M.x;
@@ -876,7 +911,24 @@ __device__ __forceinline__ void pair_consume_x2(const double (&a0)[4], const dou
     constexpr bool COS = MODE == PM_HIST_CM_COS;
     constexpr bool LAB = MODE == PM_MASS || MODE == PM_HIST;
     double c0, c1, M0, M1;
-    if constexpr (LAB) {
+    if constexpr (MODE == PM_BOTH) {
+      double C0, C1;  // CM masses
+      both_masses_fast(a0[0], a0[1], a0[2], a0[3], b0[0], b0[1], b0[2], b0[3], M0, C0);
+      both_masses_fast(a1[0], a1[1], a1[2], a1[3], b1[0], b1[1], b1[2], b1[3], M1, C1);
+      atomicAdd(&sh_hist[find_bin(M0, hp)], 1u);
+      atomicAdd(&sh_hist[find_bin(M1, hp)], 1u);
+      atomicAdd(&sh_cos[find_bin(C0, co.hc)], 1u);
+      atomicAdd(&sh_cos[find_bin(C1, co.hc)], 1u);
+      if (m_out) {
+        m_out[i0] = M0;
+        m_out[i1] = M1;
+      }
+      if (co.cos_out) {
+        co.cos_out[i0] = C0;
+        co.cos_out[i1] = C1;
+      }
+      return;
+    } else if constexpr (LAB) {
       M0 = pair_mass_fast(a0[0], a0[1], a0[2], a0[3], b0[0], b0[1], b0[2], b0[3]);
       M1 = pair_mass_fast(a1[0], a1[1], a1[2], a1[3], b1[0], b1[1], b1[2], b1[3]);
       if constexpr (MODE == PM_MASS) {
@@ -927,7 +979,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb2 = hp.nbins + 2;
   // cos theta* mode: the angle histogram follows the mass histogram in shared memory
-  const int nbt = nb2 + (MODE == PM_HIST_CM_COS ? co.hc.nbins + 2 : 0);
+  const int nbt = nb2 + ((MODE == PM_HIST_CM_COS || MODE == PM_BOTH) ? co.hc.nbins + 2 : 0);
   unsigned int* sh_cos = sh_hist + nb2;
 
   if constexpr (MODE != PM_MASS) {

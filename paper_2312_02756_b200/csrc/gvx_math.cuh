@@ -279,12 +279,10 @@ __device__ __forceinline__ bool fast_domain(float pt, float eta, float phi, floa
          (abs_bits(pt) - 0x2B800000u < 0x49800000u - 0x2B800000u) & (abs_bits(m) < 0x49800000u);
 }
 
-__device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double phi1, double m1, double pt2,
-                                                 double eta2, double phi2, double m2) {
-  double c = fast_cos(phi1 - phi2);
-  double sh1, ch1, sh2, ch2;
-  sinh_cosh(eta1, sh1, ch1);
-  sinh_cosh(eta2, sh2, ch2);
+// The lab pair mass from its transcendentals (c = cos(phi1 - phi2), sinh/cosh of
+// both etas) — shared by pair_mass_fast and the fused lab + CM pass.
+__device__ __forceinline__ double pair_mass_from(double pt1, double m1, double pt2, double m2, double c, double sh1,
+                                                 double ch1, double sh2, double ch2) {
   double q1 = pt1 * ch1, q2 = pt2 * ch2;
   double P1 = q1 * q1, P2 = q2 * q2;
   double mm1 = m1 * fabs(m1), mm2 = m2 * fabs(m2);
@@ -295,6 +293,15 @@ __device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double
   double A12 = (c1 | c2) ? 0.0 : A1 * A2;
   double m2sq = t + 2.0 * (fast_sqrt(A12) - pt1 * pt2 * (c + sh1 * sh2));
   return copy_sign_bit(fast_sqrt_abs(m2sq), m2sq);
+}
+
+__device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double phi1, double m1, double pt2,
+                                                 double eta2, double phi2, double m2) {
+  double c = fast_cos(phi1 - phi2);
+  double sh1, ch1, sh2, ch2;
+  sinh_cosh(eta1, sh1, ch1);
+  sinh_cosh(eta2, sh2, ch2);
+  return pair_mass_from(pt1, m1, pt2, m2, c, sh1, ch1, sh2, ch2);
 }
 
 // fp32: MUFU-based cos/exp/rcp/sqrt (error budget DESIGN.md §5: <= ~1e-6 E^2
@@ -513,6 +520,32 @@ template <typename V, bool WANT_COS, bool WANT_VEC>
 __device__ __forceinline__ V cm_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt2, V eta2, V phi2, V m2,
                                                V* cos_out, V* vec_out);
 
+// The CM mass in the rotated frame from its transcendentals (sd, cd = sin/cos of
+// phi2 - phi1; sinh/cosh of both etas) — shared with the fused lab + CM pass.
+template <typename T, bool WANT_COS = false>
+__device__ __forceinline__ T cm_mass_from(T pt1, T m1, T pt2, T m2, T sd, T cd, T sh1, T ch1, T sh2, T ch2,
+                                          V4<T>* a_out, V4<T>* b_out, T* cos_out) {
+  T q1 = pt1 * ch1, q2 = pt2 * ch2;
+  V4<T> a{pt1, T(0), pt1 * sh1, pos_sqrt(m1 * fabs(m1) + q1 * q1)};
+  V4<T> b{pt2 * cd, pt2 * sd, pt2 * sh2, pos_sqrt(m2 * fabs(m2) + q2 * q2)};
+  return cm_pair_mass<T, true, WANT_COS>(a, b, a_out, b_out, cos_out);
+}
+
+// Fused lab + CM masses of one fast-domain fp64 pair: the sinh/cosh of both etas
+// are evaluated once; the lab mass keeps its own cos(phi1 - phi2) (fast_cos) so
+// both results are bit-identical to pair_mass_fast and cm_mass_ptetaphim_fast.
+__device__ __forceinline__ void both_masses_fast(double pt1, double eta1, double phi1, double m1, double pt2,
+                                                 double eta2, double phi2, double m2, double& m_lab,
+                                                 double& m_cm) {
+  double sd, cd, sh1, ch1, sh2, ch2;
+  const double c = fast_cos(phi1 - phi2);
+  fast_sincos(phi2 - phi1, sd, cd);
+  sinh_cosh(eta1, sh1, ch1);
+  sinh_cosh(eta2, sh2, ch2);
+  m_lab = pair_mass_from(pt1, m1, pt2, m2, c, sh1, ch1, sh2, ch2);
+  m_cm = cm_mass_from<double, false>(pt1, m1, pt2, m2, sd, cd, sh1, ch1, sh2, ch2, nullptr, nullptr, nullptr);
+}
+
 template <typename T, bool WANT_COS = false>
 __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1, T pt2, T eta2, T phi2, T m2,
                                                     V4<T>* a_out, V4<T>* b_out, T* cos_out = nullptr) {
@@ -543,10 +576,7 @@ __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1,
   fast_sincos(phi2 - phi1, sd, cd);
   sinh_cosh(eta1, sh1, ch1);
   sinh_cosh(eta2, sh2, ch2);
-  T q1 = pt1 * ch1, q2 = pt2 * ch2;
-  V4<T> a{pt1, T(0), pt1 * sh1, pos_sqrt(m1 * fabs(m1) + q1 * q1)};
-  V4<T> b{pt2 * cd, pt2 * sd, pt2 * sh2, pos_sqrt(m2 * fabs(m2) + q2 * q2)};
-  T M = cm_pair_mass<T, true, WANT_COS>(a, b, a_out, b_out, cos_out);
+  T M = cm_mass_from<T, WANT_COS>(pt1, m1, pt2, m2, sd, cd, sh1, ch1, sh2, ch2, a_out, b_out, cos_out);
   if (a_out) {
     T s1, c1;
     fast_sincos(phi1, s1, c1);

@@ -1052,3 +1052,34 @@ def test_boost_high_beta_f64(gvx, O):
     ref, S = O.boost(v, beta)
     out = host(gvx.boost(dev(v), dev(beta)))
     assert boost_violations(out, ref, S, 1e-12).size == 0
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("layout", ["aos", "soa", "pairs"])
+def test_pair_histograms_fused_equals_separate(gvx, dt, layout):
+    """gvx_pair_histograms (one pass) == invariant_mass + mass_histogram + mass_histogram(cm),
+    bit for bit: masses, lab bins, CM masses, CM bins — TMA two-event ring (AoS/SoA, n above the
+    small-batch threshold) and the two-pass fallback (strided pairs); edge rows included."""
+    n = 300_000 + 7
+    v1, v2 = mixed_inputs(n, dt, seed=5)
+    t1, t2 = dev(v1), dev(v2)
+    if layout == "soa":
+        a = [t1[:, k].contiguous() for k in range(4)]
+        b = [t2[:, k].contiguous() for k in range(4)]
+    elif layout == "pairs":
+        pr = torch.stack([t1, t2], 1).contiguous()
+        a, b = pr[:, 0], pr[:, 1]
+    else:
+        a, b = t1, t2
+    N = v1.shape[0]
+    m, mc = (torch.empty(N, dtype=TDT[dt], device="cuda") for _ in range(2))
+    lab, cmb = gvx.pair_histograms(a, b, m_out=m, cm_m_out=mc)
+    m_ref = gvx.invariant_mass(t1, t2)
+    mc_ref = torch.empty_like(m_ref)
+    h_ref = gvx.mass_histogram(t1, t2)
+    hc_ref = gvx.mass_histogram(t1, t2, cm=True, m_out=mc_ref)
+    assert torch.equal(lab, h_ref) and torch.equal(cmb, hc_ref)
+    assert np.array_equal(host(m), host(m_ref), equal_nan=True)
+    assert np.array_equal(host(mc), host(mc_ref), equal_nan=True)
+    lab2, cmb2 = gvx.pair_histograms(a, b, lab_bins=lab.clone(), cm_bins=cmb.clone())  # accumulates
+    assert torch.equal(lab2, 2 * h_ref) and torch.equal(cmb2, 2 * hc_ref)

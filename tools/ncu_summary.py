@@ -40,7 +40,8 @@ def kernel_key(name: str):
     cm = None
     if "k_pair_tma" in name:
         mode = name.split("k_pair_tma<")[1].split(",")[2].strip()
-        return {"0": "invariant_mass", "1": "mass_histogram", "2": "mass_histogram_cm", "3": "cm_costheta_hist"}[mode]
+        return {"0": "invariant_mass", "1": "mass_histogram", "2": "mass_histogram_cm", "3": "cm_costheta_hist",
+                "4": "pairs"}[mode]
     if "k_cm_costheta" in name:
         return "cm_costheta_hist"
     if "k_invariant_mass" in name:
@@ -56,7 +57,7 @@ def main():
     n = int(float(sys.argv[4])) if len(sys.argv) > 4 else 100_000_000
     es = 8 if dtype == "f64" else 4
     algo = {"invariant_mass": 9 * es, "boost": 11 * es, "mass_histogram": 8 * es, "mass_histogram_cm": 8 * es,
-            "cm_costheta_hist": 8 * es}
+            "cm_costheta_hist": 8 * es, "pairs": 9 * es}
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, units = rows[0], rows[1]

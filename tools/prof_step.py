@@ -35,5 +35,6 @@ for _ in range(a.reps):
     gvx.mass_histogram(v1, v2, bins=bins)
     gvx.mass_histogram(v1, v2, bins=bins, cm=True)
     gvx.cm_costheta_histogram(v1, v2)
+    gvx.pair_histograms(v1, v2, m_out=m)
 torch.cuda.synchronize()
 print("prof_step done")
