@@ -297,7 +297,10 @@ __device__ __forceinline__ double pair_mass_from(double pt1, double m1, double p
 
 __device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double phi1, double m1, double pt2,
                                                  double eta2, double phi2, double m2) {
-  double c = fast_cos(phi1 - phi2);
+  // cos(phi1 - phi2) is taken from the same sincos(phi2 - phi1) the CM mass
+  // uses, so the fused lab + CM pass evaluates one trigonometric reduction.
+  double sd, c;
+  fast_sincos(phi2 - phi1, sd, c);
   double sh1, ch1, sh2, ch2;
   sinh_cosh(eta1, sh1, ch1);
   sinh_cosh(eta2, sh2, ch2);
@@ -532,17 +535,17 @@ __device__ __forceinline__ T cm_mass_from(T pt1, T m1, T pt2, T m2, T sd, T cd, 
 }
 
 // Fused lab + CM masses of one fast-domain fp64 pair: the sinh/cosh of both etas
-// are evaluated once; the lab mass keeps its own cos(phi1 - phi2) (fast_cos) so
+// and the sincos of phi2 - phi1 are evaluated once (the lab mass takes the same
+// cos as pair_mass_fast) so
 // both results are bit-identical to pair_mass_fast and cm_mass_ptetaphim_fast.
 __device__ __forceinline__ void both_masses_fast(double pt1, double eta1, double phi1, double m1, double pt2,
                                                  double eta2, double phi2, double m2, double& m_lab,
                                                  double& m_cm) {
   double sd, cd, sh1, ch1, sh2, ch2;
-  const double c = fast_cos(phi1 - phi2);
   fast_sincos(phi2 - phi1, sd, cd);
   sinh_cosh(eta1, sh1, ch1);
   sinh_cosh(eta2, sh2, ch2);
-  m_lab = pair_mass_from(pt1, m1, pt2, m2, c, sh1, ch1, sh2, ch2);
+  m_lab = pair_mass_from(pt1, m1, pt2, m2, cd, sh1, ch1, sh2, ch2);
   m_cm = cm_mass_from<double, false>(pt1, m1, pt2, m2, sd, cd, sh1, ch1, sh2, ch2, nullptr, nullptr, nullptr);
 }
 
@@ -644,7 +647,9 @@ template <typename V>
 __device__ __forceinline__ V pair_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt2, V eta2, V phi2, V m2) {
   const V MONE = lv_splat(V{}, -1.f), HALF = lv_splat(V{}, 0.5f), TWO = lv_splat(V{}, 2.f);
   const V LOG2E = lv_splat(V{}, 1.44269504088896341f);
-  V d = lv_fma(phi2, MONE, phi1);
+  // cos(phi2 - phi1) = cos(phi1 - phi2), reduced exactly as cm_mass_f32_lanes
+  // does, so the fused lab + CM pass shares the reduction and the MUFU.COS
+  V d = lv_fma(phi1, MONE, phi2);
   V k = lv_map(lv_mul(d, lv_splat(V{}, 0.159154943091895336f)), [](float x) { return rintf(x); });
   V r = lv_fma(k, lv_splat(V{}, -6.28318548202514648f), d);
   r = lv_fma(k, lv_splat(V{}, 1.74845553146951715e-7f), r);
