@@ -279,19 +279,24 @@ __device__ __forceinline__ bool fast_domain(float pt, float eta, float phi, floa
          (abs_bits(pt) - 0x2B800000u < 0x49800000u - 0x2B800000u) & (abs_bits(m) < 0x49800000u);
 }
 
-// The lab pair mass from its transcendentals (c = cos(phi1 - phi2), sinh/cosh of
-// both etas) — shared by pair_mass_fast and the fused lab + CM pass.
+// E = sqrt(max(0, (pt cosh eta)^2 + m|m|)) of a PtEtaPhiM vector from q = pt cosh eta
+// (the R2 clamp comes from fast_sqrt / pos_sqrt) — one expression shared by the lab
+// and the CM mass, so the fused pass evaluates it once per vector.
+template <typename T>
+__device__ __forceinline__ T energy_of(T m, T q);
+
+// The lab pair mass from its transcendentals and energies (c = cos(phi1 - phi2),
+// sinh of both etas, q = pt cosh eta, E from energy_of) — shared by pair_mass_fast
+// and the fused lab + CM pass:
+//   M^2 = t1 + t2 + 2 (E1 E2 - pt1 pt2 (c + sh1 sh2)),  t = m|m| (E^2 - |p|^2),
+// or t = -q^2 for a clamped vector (E^2 < 0 -> E = 0, reading R2).
 __device__ __forceinline__ double pair_mass_from(double pt1, double m1, double pt2, double m2, double c, double sh1,
-                                                 double ch1, double sh2, double ch2) {
-  double q1 = pt1 * ch1, q2 = pt2 * ch2;
-  double P1 = q1 * q1, P2 = q2 * q2;
+                                                 double sh2, double q1, double q2, double E1, double E2) {
   double mm1 = m1 * fabs(m1), mm2 = m2 * fabs(m2);
-  double A1 = mm1 + P1, A2 = mm2 + P2;
-  // E^2 clamp (R2): a clamped vector has E = 0 and E^2 - |p|^2 = -P.
-  bool c1 = A1 < 0.0, c2 = A2 < 0.0;
-  double t = (c1 ? -P1 : mm1) + (c2 ? -P2 : mm2);
-  double A12 = (c1 | c2) ? 0.0 : A1 * A2;
-  double m2sq = t + 2.0 * (fast_sqrt(A12) - pt1 * pt2 * (c + sh1 * sh2));
+  // clamp test on the sign bit of E^2 (integer op; E^2 = -0 is impossible: q >= pt > 0)
+  bool c1 = __double2hiint(fma(q1, q1, mm1)) < 0, c2 = __double2hiint(fma(q2, q2, mm2)) < 0;
+  double t = (c1 ? -(q1 * q1) : mm1) + (c2 ? -(q2 * q2) : mm2);
+  double m2sq = t + 2.0 * (E1 * E2 - pt1 * pt2 * (c + sh1 * sh2));
   return copy_sign_bit(fast_sqrt_abs(m2sq), m2sq);
 }
 
@@ -304,7 +309,8 @@ __device__ __forceinline__ double pair_mass_fast(double pt1, double eta1, double
   double sh1, ch1, sh2, ch2;
   sinh_cosh(eta1, sh1, ch1);
   sinh_cosh(eta2, sh2, ch2);
-  return pair_mass_from(pt1, m1, pt2, m2, c, sh1, ch1, sh2, ch2);
+  double q1 = pt1 * ch1, q2 = pt2 * ch2;
+  return pair_mass_from(pt1, m1, pt2, m2, c, sh1, sh2, q1, q2, energy_of(m1, q1), energy_of(m2, q2));
 }
 
 // fp32: MUFU-based cos/exp/rcp/sqrt (error budget DESIGN.md §5: <= ~1e-6 E^2
@@ -523,21 +529,24 @@ template <typename V, bool WANT_COS, bool WANT_VEC>
 __device__ __forceinline__ V cm_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt2, V eta2, V phi2, V m2,
                                                V* cos_out, V* vec_out);
 
+template <typename T>
+__device__ __forceinline__ T energy_of(T m, T q) {
+  return pos_sqrt(fma(q, q, m * fabs(m)));
+}
+
 // The CM mass in the rotated frame from its transcendentals (sd, cd = sin/cos of
-// phi2 - phi1; sinh/cosh of both etas) — shared with the fused lab + CM pass.
+// phi2 - phi1; sinh of both etas) and energies — shared with the fused lab + CM pass.
 template <typename T, bool WANT_COS = false>
-__device__ __forceinline__ T cm_mass_from(T pt1, T m1, T pt2, T m2, T sd, T cd, T sh1, T ch1, T sh2, T ch2,
-                                          V4<T>* a_out, V4<T>* b_out, T* cos_out) {
-  T q1 = pt1 * ch1, q2 = pt2 * ch2;
-  V4<T> a{pt1, T(0), pt1 * sh1, pos_sqrt(m1 * fabs(m1) + q1 * q1)};
-  V4<T> b{pt2 * cd, pt2 * sd, pt2 * sh2, pos_sqrt(m2 * fabs(m2) + q2 * q2)};
+__device__ __forceinline__ T cm_mass_from(T pt1, T pt2, T sd, T cd, T sh1, T sh2, T E1, T E2, V4<T>* a_out,
+                                          V4<T>* b_out, T* cos_out) {
+  V4<T> a{pt1, T(0), pt1 * sh1, E1};
+  V4<T> b{pt2 * cd, pt2 * sd, pt2 * sh2, E2};
   return cm_pair_mass<T, true, WANT_COS>(a, b, a_out, b_out, cos_out);
 }
 
-// Fused lab + CM masses of one fast-domain fp64 pair: the sinh/cosh of both etas
-// and the sincos of phi2 - phi1 are evaluated once (the lab mass takes the same
-// cos as pair_mass_fast) so
-// both results are bit-identical to pair_mass_fast and cm_mass_ptetaphim_fast.
+// Fused lab + CM masses of one fast-domain fp64 pair: sinh/cosh of both etas,
+// the sincos of phi2 - phi1 and both energies are evaluated once; both results are
+// bit-identical to pair_mass_fast and cm_mass_ptetaphim_fast.
 __device__ __forceinline__ void both_masses_fast(double pt1, double eta1, double phi1, double m1, double pt2,
                                                  double eta2, double phi2, double m2, double& m_lab,
                                                  double& m_cm) {
@@ -545,8 +554,10 @@ __device__ __forceinline__ void both_masses_fast(double pt1, double eta1, double
   fast_sincos(phi2 - phi1, sd, cd);
   sinh_cosh(eta1, sh1, ch1);
   sinh_cosh(eta2, sh2, ch2);
-  m_lab = pair_mass_from(pt1, m1, pt2, m2, cd, sh1, ch1, sh2, ch2);
-  m_cm = cm_mass_from<double, false>(pt1, m1, pt2, m2, sd, cd, sh1, ch1, sh2, ch2, nullptr, nullptr, nullptr);
+  const double q1 = pt1 * ch1, q2 = pt2 * ch2;
+  const double E1 = energy_of(m1, q1), E2 = energy_of(m2, q2);
+  m_lab = pair_mass_from(pt1, m1, pt2, m2, cd, sh1, sh2, q1, q2, E1, E2);
+  m_cm = cm_mass_from<double, false>(pt1, pt2, sd, cd, sh1, sh2, E1, E2, nullptr, nullptr, nullptr);
 }
 
 template <typename T, bool WANT_COS = false>
@@ -579,7 +590,9 @@ __device__ __forceinline__ T cm_mass_ptetaphim_fast(T pt1, T eta1, T phi1, T m1,
   fast_sincos(phi2 - phi1, sd, cd);
   sinh_cosh(eta1, sh1, ch1);
   sinh_cosh(eta2, sh2, ch2);
-  T M = cm_mass_from<T, WANT_COS>(pt1, m1, pt2, m2, sd, cd, sh1, ch1, sh2, ch2, a_out, b_out, cos_out);
+  T q1 = pt1 * ch1, q2 = pt2 * ch2;
+  T M = cm_mass_from<T, WANT_COS>(pt1, pt2, sd, cd, sh1, sh2, energy_of(m1, q1), energy_of(m2, q2), a_out, b_out,
+                                  cos_out);
   if (a_out) {
     T s1, c1;
     fast_sincos(phi1, s1, c1);
