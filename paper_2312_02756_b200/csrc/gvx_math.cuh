@@ -709,9 +709,10 @@ __device__ __forceinline__ V cm_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt
   auto pos_sqrt_f = [](float x) { return fast_sqrt(x > 0.f ? x : 0.f); };
   // vector 1 in the rotated frame: (pt1, 0, pt1 sh1, E1); vector 2: (pt2 cd, pt2 sd, pt2 sh2, E2)
   V ax = pt1, az = lv_mul(pt1, sh1);
-  V aE = lv_map(lv_fma(m1, lv_map(m1, [](float x) { return fabsf(x); }), lv_mul(q1, q1)), pos_sqrt_f);
+  // E = sqrt(max(0, q^2 + m|m|)), the same expression as pair_mass_f32_lanes (shared in the fused pass)
+  V aE = lv_map(lv_fma(q1, q1, lv_mul(m1, lv_map(m1, [](float x) { return fabsf(x); }))), pos_sqrt_f);
   V bx = lv_mul(pt2, cd), by = lv_mul(pt2, sd), bz = lv_mul(pt2, sh2);
-  V bE = lv_map(lv_fma(m2, lv_map(m2, [](float x) { return fabsf(x); }), lv_mul(q2, q2)), pos_sqrt_f);
+  V bE = lv_map(lv_fma(q2, q2, lv_mul(m2, lv_map(m2, [](float x) { return fabsf(x); }))), pos_sqrt_f);
   // beta_cm = -P / E (P_y = b_y: vector 1 has no y component in this frame)
   // every sum whose operand is a product is an explicit fma: ptxas contracts
   // mul.rn.f32x2 + add.rn.f32x2 pairs (unlike the scalar .rn forms), which
