@@ -996,6 +996,40 @@ def test_bench_step_histograms_full_size(gvx, O, dt):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_bench_step_fused_pass_full_size(gvx, O, dt):
+    """The bench step's fused pair pass (gvx_pair_histograms) at its size and launch
+    configuration (1e8 pairs, two-event TMA ring): both histograms == FindBin of the kernel's own
+    lab / CM masses over all 1e8 events, sampled lab and CM masses vs the oracle, and the
+    histograms and masses equal to the separate kernels' bit for bit."""
+    import synth.device as sd
+    n = 100_000_000
+    v1, v2 = sd.muon_pairs(n, dtype=TDT[dt])
+    m, mc = (torch.empty(n, dtype=TDT[dt], device="cuda") for _ in range(2))
+    lab, cmb = gvx.pair_histograms(v1, v2, m_out=m, cm_m_out=mc)
+    for h, mm in ((lab, m), (cmb, mc)):
+        assert int(h.sum()) == n
+        x = mm.double()
+        q = (float(NB) * (x - LO)) / (HI - LO)
+        inner = 1 + torch.trunc(torch.nan_to_num(q, nan=0.0, posinf=0.0, neginf=0.0)).long()
+        bb = torch.where(x < LO, 0, torch.where(~(x < HI), NB + 1, inner))
+        assert torch.equal(torch.bincount(bb, minlength=NB + 2), h)
+        del x, q, inner, bb
+    idx = _sample_idx(n, seed=17)
+    a, b = synth.muon_pairs(idx, dtype=dt)
+    sel = torch.from_numpy(idx).cuda()
+    tau = tau_of(dt)
+    mlab, e = O.invariant_mass(a, b)
+    mo, ec = O.cm_mass(a, b)
+    assert mass_violations(host(m[sel]), mlab, e, tau).size == 0
+    ok = np.isfinite(mo) & (np.abs(mlab.astype(np.float64)) >= (1e-2 if dt == np.float32 else 1e-6) * e)
+    assert mass_violations(host(mc[sel])[ok], mo[ok], ec[ok], tau).size == 0
+    ref = torch.empty_like(m)
+    bits = (lambda t: t.view(torch.int64)) if dt == np.float64 else (lambda t: t.view(torch.int32))
+    assert torch.equal(gvx.mass_histogram(v1, v2, m_out=ref), lab) and torch.equal(bits(ref), bits(m))
+    assert torch.equal(gvx.mass_histogram(v1, v2, cm=True, m_out=ref), cmb) and torch.equal(bits(ref), bits(mc))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_fast_domain_edges(gvx, O, dt):
     """Inputs just inside (and just outside) the fast-path domain of the GPU arithmetic
     (|eta| < 20, |phi| < 1024 f64 / 8 f32, 2^-200 (f64) / 2^-40 (f32) <= pt, pt and |m| large):
