@@ -105,6 +105,28 @@ def test_cm_costheta_validation(gvx):
     assert call(n=0, m=(1.0, 1.0, 10)) == 1               # ... but a bad axis is still an error
 
 
+def test_pair_histograms_validation(gvx):
+    """gvx_pair_histograms (ABI v5) validates the axis, both bin arrays and the optional mass
+    outputs synchronously; n == 0 is OK with nothing launched."""
+    L = gvx.lib
+    by = ctypes.byref
+    a, b = _view(), _view()
+    P = L.gvx_pair_histograms
+
+    def call(n=4, ax=(0.25, 300.0, 1000), lb=0x4000, cb=0x5000, mo=None, co=None, dt=gvx.GVX_F64, coords=0):
+        return P(dt, coords, by(a), by(b), n, ax[0], ax[1], ax[2], lb, cb, mo, co, None)
+
+    assert call(ax=(1.0, 1.0, 10)) == 1                   # lo >= hi
+    assert call(ax=(float("-inf"), 1.0, 10)) == 1         # non-finite edge
+    assert call(ax=(0.0, 1.0, 0)) == 1 and call(ax=(0.0, 1.0, 1 << 29)) == 1
+    assert call(lb=None) == 1 and call(cb=None) == 1      # missing bins
+    assert call(lb=0x4004) == 1 and call(cb=0x5002) == 1  # misaligned bins
+    assert call(mo=0x6001) == 1 and call(co=0x7003) == 1  # misaligned mass outputs
+    assert call(dt=7) == 1 and call(coords=9) == 1 and call(n=-1) == 1
+    assert call(n=0, lb=None, cb=None) == 0               # n == 0: OK, nothing launched
+    assert call(n=0, ax=(1.0, 1.0, 10)) == 1              # ... but a bad axis is still an error
+
+
 def test_mass_histogram_peers_validation(gvx):
     """The fused-reduction entry point (ABI v4) checks its sink arguments synchronously."""
     L = gvx.lib

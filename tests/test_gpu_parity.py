@@ -1117,3 +1117,49 @@ def test_pair_histograms_fused_equals_separate(gvx, dt, layout):
     assert np.array_equal(host(mc), host(mc_ref), equal_nan=True)
     lab2, cmb2 = gvx.pair_histograms(a, b, lab_bins=lab.clone(), cm_bins=cmb.clone())  # accumulates
     assert torch.equal(lab2, 2 * h_ref) and torch.equal(cmb2, 2 * hc_ref)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("case", ["pxpypze", "pxpypzm", "wide_axis", "small_n", "empty", "ragged_ring"])
+def test_pair_histograms_other_branches(gvx, dt, case):
+    """The fused pass's other dispatch branches equal the separate kernels bit for bit:
+    Cartesian input through the TMA ring (PxPyPzE) and the two-pass fallback (PxPyPzM), an axis
+    too wide for two shared-memory histograms (nbins = 40000: fallback), a batch below the
+    small-batch threshold, n = 0 (nothing launched, bins untouched) and a ring whose last stage
+    is ragged (n = one stage x 148 CTAs + 1)."""
+    coords, nb, n = "ptetaphim", NB, 300_007
+    if case in ("pxpypze", "pxpypzm"):
+        coords = case
+    elif case == "wide_axis":
+        nb = 40_000
+    elif case == "small_n":
+        n = 1_001
+    elif case == "empty":
+        n = 0
+    elif case == "ragged_ring":
+        n = (1536 if dt == np.float64 else 1792) * 148 + 1
+    if coords == "ptetaphim":
+        v1, v2 = mixed_inputs(max(n, 1), dt, seed=9)
+        v1, v2 = v1[:n], v2[:n]
+    else:
+        v1, _ = synth.boost_inputs(np.arange(n), dtype=dt, seed=5)
+        v2, _ = synth.boost_inputs(np.arange(n), dtype=dt, seed=6)
+        if coords == "pxpypzm":  # same momenta, the 4th component the (signed) mass
+            for v in (v1, v2):
+                v[:, 3] = np.sqrt(np.maximum(v[:, 3] ** 2 - (v[:, :3] ** 2).sum(1), 0.0))
+    t1, t2 = dev(v1), dev(v2)
+    N = t1.shape[0]
+    m, mc = (torch.empty(N, dtype=TDT[dt], device="cuda") for _ in range(2))
+    lab0 = torch.arange(nb + 2, dtype=torch.int64, device="cuda")
+    lab, cmb = gvx.pair_histograms(t1, t2, LO, HI, nb, lab_bins=lab0.clone(), cm_bins=lab0.clone(), m_out=m,
+                                   cm_m_out=mc, coords=coords)
+    m_ref, mc_ref = torch.empty_like(m), torch.empty_like(mc)
+    h_ref = gvx.mass_histogram(t1, t2, LO, HI, nb, bins=lab0.clone(), m_out=m_ref, coords=coords)
+    hc_ref = gvx.mass_histogram(t1, t2, LO, HI, nb, cm=True, bins=lab0.clone(), m_out=mc_ref, coords=coords)
+    assert torch.equal(lab, h_ref) and torch.equal(cmb, hc_ref)
+    assert np.array_equal(host(m), host(m_ref), equal_nan=True)
+    assert np.array_equal(host(mc), host(mc_ref), equal_nan=True)
+    if n == 0:
+        assert torch.equal(lab, lab0) and torch.equal(cmb, lab0)
+    else:
+        assert int((lab - lab0).sum()) == n and int((cmb - lab0).sum()) == n
