@@ -333,8 +333,9 @@ def run_ours(args):
     bv, bb = sd.boost_inputs(n, first=first, dtype=tdt, device=dev)
     m = torch.empty(n, dtype=tdt, device=dev)
     bout = torch.empty((n, 4), dtype=tdt, device=dev)
-    bins = gvx.new_bins(NB, dev)
-    bins_cm = gvx.new_bins(NB, dev)
+    # both histograms in one int64 buffer: one memset and, for N > 1, ONE all-reduce per step
+    bins_all = torch.zeros(2 * (NB + 2), dtype=torch.int64, device=dev)
+    bins, bins_cm = bins_all[:NB + 2], bins_all[NB + 2:]
     torch.cuda.synchronize(dev)
 
     p2p = world > 1 and args.bin_reduce == "p2p" and args.dist_backend == "nccl"
@@ -344,8 +345,7 @@ def run_ours(args):
     kern_ms = {k: [] for k in order}
 
     def step(record: bool):
-        bins.zero_()
-        bins_cm.zero_()
+        bins_all.zero_()
         if record:
             ev[0].record(stream)
         if fused:
@@ -356,8 +356,7 @@ def run_ours(args):
             if record:
                 ev[2].record(stream)
             if world > 1:
-                gvx.allreduce_bins(bins)
-                gvx.allreduce_bins(bins_cm)
+                gvx.allreduce_bins(bins_all)
             return
         gvx.invariant_mass(v1, v2, out=m)
         if record:
@@ -380,8 +379,7 @@ def run_ours(args):
         if record:
             ev[4].record(stream)
         if world > 1:
-            gvx.allreduce_bins(bins)
-            gvx.allreduce_bins(bins_cm)
+            gvx.allreduce_bins(bins_all)
 
     for _ in range(args.warmup):
         step(False)
