@@ -37,14 +37,22 @@ BYTES = {
     "mass_histogram": lambda es: 8 * es,           # two vectors in (bins: per-call constant)
     "mass_histogram_cm": lambda es: 8 * es,
     "pairs": lambda es: 8 * es + es,               # fused pass: pairs in once, lab masses out
+    "step": lambda es: 8 * es + es + 11 * es,      # one launch: the fused pass + the boost
 }
 KERNEL_ORDER = ["invariant_mass", "boost", "mass_histogram", "mass_histogram_cm"]
 # The default step: gvx_pair_histograms (lab mass + lab histogram + CM mass + CM histogram in ONE
 # pass over the pairs, bit-identical to the three separate kernels) and the boost.
 FUSED_ORDER = ["pairs", "boost"]
+# f64 default: the whole step in ONE launch (gvx_pair_histograms_boost: pair ring + boost ring on
+# every SM, bit-identical to the two calls); --two-launch times FUSED_ORDER instead.
+STEP_ORDER = ["step"]
 # Λ(β = (0, 0, 0.6)) · R_z(0.7): a general Lorentz transformation for the --extended timing
 _c, _s, _g = 0.7648421872844885, 0.644217687237691, 1.25
 LORENTZ_DEMO = [[_c, -_s, 0, 0], [_s, _c, 0, 0], [0, 0, _g, _g * 0.6], [0, 0, _g * 0.6, _g]]
+
+
+def one_launch_step(args) -> bool:
+    return args.dtype == "f64" and not getattr(args, "two_launch", False) and not getattr(args, "unfused", False)
 
 
 def parse():
@@ -59,6 +67,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=1 << 22, help="events in the oracle's bounded sample")
     p.add_argument("--dist-backend", default="nccl", help="process-group backend for N>1 (nccl on B200s)")
+    p.add_argument("--two-launch", action="store_true",
+                   help="f64: time the fused pair pass and the boost as two launches instead of one")
     p.add_argument("--unfused", action="store_true",
                    help="time the step as four kernels (mass, boost, lab histogram, CM histogram) instead of the "
                         "fused pair pass + boost")
@@ -230,6 +240,9 @@ def config_obj(args, world, ref_sample=None):
              if world > 1 and getattr(args, "bin_reduce", "nccl") == "p2p" and getattr(args, "dist_backend", "nccl") == "nccl"
              else f"{getattr(args, 'dist_backend', 'nccl')} bin all-reduce)")}
     c["kernels"] = ("four kernels: mass, boost, lab histogram, CM histogram" if getattr(args, "unfused", False)
+                    else "gvx_pair_histograms_boost: ONE launch doing the fused pair pass (lab mass + lab histogram "
+                         "+ CM mass + CM histogram in one read of the pairs) and the boost, bit-identical to the "
+                         "separate kernels" if one_launch_step(args)
                     else "gvx_pair_histograms (lab mass + lab histogram + CM mass + CM histogram in one pass over "
                          "the pairs, bit-identical to the separate kernels) + boost")
     if ref_sample:
@@ -340,7 +353,8 @@ def run_ours(args):
 
     p2p = world > 1 and args.bin_reduce == "p2p" and args.dist_backend == "nccl"
     fused = not args.unfused and not p2p
-    order = FUSED_ORDER if fused else KERNEL_ORDER
+    one = fused and one_launch_step(args)
+    order = STEP_ORDER if one else FUSED_ORDER if fused else KERNEL_ORDER
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(order) + 1)]
     kern_ms = {k: [] for k in order}
 
@@ -348,6 +362,13 @@ def run_ours(args):
         bins_all.zero_()
         if record:
             ev[0].record(stream)
+        if one:
+            gvx.pair_histograms_boost(v1, v2, bv, bb, LO, HI, NB, lab_bins=bins, cm_bins=bins_cm, m_out=m, out=bout)
+            if record:
+                ev[1].record(stream)
+            if world > 1:
+                gvx.allreduce_bins(bins_all)
+            return
         if fused:
             gvx.pair_histograms(v1, v2, LO, HI, NB, lab_bins=bins, cm_bins=bins_cm, m_out=m)
             if record:
@@ -426,6 +447,9 @@ def run_ours(args):
                 "unit": "GB/s", "frac": kernels[dom]["frac_of_peak"], "traffic": ncu_traffic(dom, args.dtype, n),
                 "peak_source": peak_kind,
                 "bytes_per_launch": n * BYTES[dom](es)}
+    if dom == "step":
+        roofline["note"] = ("one launch streams the pairs (FP64-bound fused pass) and the boost inputs (HBM-bound) "
+                            "on every SM at once; --two-launch times them separately")
     if dom == "pairs":
         roofline["note"] = ("the fused pass moves 1/3 of the unfused pair bytes; it is bound by arithmetic "
                             "(f64: FP64 pipe; f32: issue + MUFU), see profiles/r01/ncu_summary_*.md; "

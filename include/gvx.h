@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define GVX_ABI_VERSION 5
+#define GVX_ABI_VERSION 6
 
 typedef struct CUstream_st *gvx_stream_t; /* == cudaStream_t */
 
@@ -172,6 +172,26 @@ gvx_status gvx_pair_histograms(gvx_dtype dtype, gvx_coords coords, const gvx_vec
                                int32_t nbins, unsigned long long *lab_bins,
                                unsigned long long *cm_bins, void *m_out, void *cm_m_out,
                                gvx_stream_t stream);
+
+/*
+ * gvx_pair_histograms_boost — the whole hot-path step of two batches in ONE
+ * persistent launch (ABI v6): gvx_pair_histograms of the n pairs (v1, v2) and
+ * gvx_boost of the nb vectors bv by their velocities beta into bout
+ * (PAPER.md:136 ApplyBoost). The pair pass is bound by
+ * the FP64 pipe and the boost by HBM, so each SM runs both at once: one TMA
+ * producer feeds a pair ring and a boost ring, pair-consumer warps and boost
+ * warps share the SM. Arguments, ownership and errors as the two calls; every
+ * output is bit-identical to gvx_pair_histograms followed by gvx_boost (which
+ * is what runs for shapes the one-launch kernel does not take: non-AoS views,
+ * non-PtEtaPhiM pairs, batches under 2^20). bout must not overlap the pair
+ * inputs or outputs.
+ */
+gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview *v1,
+                                     const gvx_vec4_cview *v2, int64_t n, double lo, double hi,
+                                     int32_t nbins, unsigned long long *lab_bins,
+                                     unsigned long long *cm_bins, void *m_out, void *cm_m_out,
+                                     const gvx_vec4_cview *bv, const gvx_vec3_cview *beta,
+                                     const gvx_vec4_view *bout, int64_t nb, gvx_stream_t stream);
 
 /*
  * gvx_mass_histogram_peers — gvx_mass_histogram with the cross-GPU bin

@@ -43,7 +43,7 @@ GVX_PXPYPZE = 1
 GVX_PXPYPZM = 2
 GVX_PTETAPHIE = 3
 GVX_HIST_BOOST_TO_CM = 0x1
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 # The default histogram of the north star: 1000 bins over the dimuon range
 # (reading R13).
@@ -103,6 +103,11 @@ def _load_lib():
     lib.gvx_pair_histograms.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P, P, P]
     lib.gvx_pair_histograms.restype = st
+    lib.gvx_pair_histograms_boost.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
+                                              ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P, P,
+                                              ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec3CView),
+                                              ctypes.POINTER(Vec4View), I64, P]
+    lib.gvx_pair_histograms_boost.restype = st
     lib.gvx_mass_histogram_peers.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
                                              ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, ctypes.c_int32,
                                              P, ctypes.c_uint32, P, P]
@@ -435,6 +440,36 @@ def pair_histograms(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = 
                                        float(lo), float(hi), int(nbins), lab_bins.data_ptr(), cm_bins.data_ptr(),
                                        mptr, cptr, _stream(dev)), "gvx_pair_histograms")
     return lab_bins, cm_bins
+
+
+def pair_histograms_boost(v1: VecArg, v2: VecArg, bv: VecArg, beta: VecArg, lo: float = DEFAULT_LO,
+                          hi: float = DEFAULT_HI, nbins: int = DEFAULT_NBINS, lab_bins: Optional[torch.Tensor] = None,
+                          cm_bins: Optional[torch.Tensor] = None, m_out: Optional[torch.Tensor] = None,
+                          cm_m_out: Optional[torch.Tensor] = None, out: Optional[VecArg] = None,
+                          coords: str = "ptetaphim"):
+    """gvx_pair_histograms_boost: pair_histograms(v1, v2) and boost(bv, beta) in ONE launch
+    (bit-identical to the two calls). Returns ``(lab_bins, cm_bins, boosted)``."""
+    a, n, dt, dev, _ = _view(v1, 4, "v1")
+    b, n2, dt2, dev2, _ = _view(v2, 4, "v2")
+    if n != n2:
+        raise ValueError(f"length mismatch: v1 has {n} vectors, v2 has {n2}")
+    c, nb, dtc, devc, _ = _view(bv, 4, "bv")
+    d, nb2, dtd, devd, _ = _view(beta, 3, "beta")
+    if nb != nb2:
+        raise ValueError(f"length mismatch: bv has {nb} vectors, beta has {nb2}")
+    if len({dt, dt2, dtc, dtd}) != 1 or len({dev, dev2, devc, devd}) != 1:
+        raise ValueError("all inputs must share dtype and device")
+    lab_bins = _bins_arg(lab_bins, nbins, dev, "lab_bins")
+    cm_bins = _bins_arg(cm_bins, nbins, dev, "cm_bins")
+    mptr = _out_1d(m_out, n, dt, "m_out")
+    cptr = _out_1d(cm_m_out, n, dt, "cm_m_out")
+    out, o = _boost_out(bv, nb, dt, dev, out)
+    with torch.cuda.device(dev):
+        _check(lib.gvx_pair_histograms_boost(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b),
+                                             n, float(lo), float(hi), int(nbins), lab_bins.data_ptr(),
+                                             cm_bins.data_ptr(), mptr, cptr, ctypes.byref(c), ctypes.byref(d),
+                                             ctypes.byref(o), nb, _stream(dev)), "gvx_pair_histograms_boost")
+    return lab_bins, cm_bins, out
 
 
 def mass_histogram_peers(v1: VecArg, v2: VecArg, peer_bins_dev: int, npeers: int, lo: float = DEFAULT_LO,

@@ -476,6 +476,41 @@ gvx_status dispatch_both(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int
   return dispatch_hist<T, C, true>(v1, v2, n, hp, cm_bins, cm_m_out, nullptr, s);
 }
 
+// ---------------------------------------------------------- one-launch step --
+template <typename T, typename CFG, typename BR>
+gvx_status launch_step(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, const HistParams& hp,
+                       unsigned long long* lab_bins, unsigned long long* cm_bins, void* m_out, void* cm_m_out,
+                       const T* bv, const T* bb, T* bout, int64_t nb, cudaStream_t s) {
+  const int nbs = 2 * (hp.nbins + 2);
+  const size_t sm = (size_t)CFG::RING_BYTES + BR::RING_BYTES + 16 * (CFG::STAGES + BR::BST) + (size_t)nbs * 4;
+  if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
+  auto k = k_step<T, CFG, BR>;
+  const int block = 32 * (CFG::NCW + 1 + BR::NBW);
+  if (blocks_per_sm(k, block, sm) < 1) return GVX_ERR_UNSUPPORTED;
+  const int grid = sm_count();
+  if (n > ((int64_t)grid << 31)) return GVX_ERR_UNSUPPORTED;  // per-CTA uint32 counters
+  CosOut<T> co{hp, cm_bins, (T*)cm_m_out};
+  co.hc.peers = nullptr;
+  co.hc.npeers = 0;
+  co.hc.mc = nullptr;
+  k<<<grid, block, sm, s>>>(mk4<T>(v1), mk4<T>(v2), n, (T*)m_out, hp, lab_bins, co, bv, bb, bout, nb);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+// AoS [N][4] rows (16-B aligned) / AoS [N][3] velocities (16-B aligned, contiguous).
+template <typename V>
+static bool aos4(const V* v, size_t es) {
+  const char* b = (const char*)v->c[0];
+  bool ok = v->stride == 4 && aligned(b, 16);
+  for (int k = 1; k < 4; ++k) ok = ok && (const char*)v->c[k] == b + k * es;
+  return ok;
+}
+static bool aos3(const gvx_vec3_cview* v, size_t es) {
+  const char* b = (const char*)v->c[0];
+  return v->stride == 3 && aligned(b, 16) && (const char*)v->c[1] == b + es && (const char*)v->c[2] == b + 2 * es;
+}
+
 // ------------------------------------------------------ cos theta* -------
 template <typename T, int C>
 gvx_status dispatch_costheta(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, const HistParams& hm,
@@ -790,6 +825,54 @@ gvx_status gvx_pair_histograms(gvx_dtype dtype, gvx_coords coords, const gvx_vec
   }
   GVX_BOTH_COORDS(float)
 #undef GVX_BOTH_COORDS
+}
+
+gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,
+                                     const gvx_vec4_cview* v2, int64_t n, double lo, double hi, int32_t nbins,
+                                     unsigned long long* lab_bins, unsigned long long* cm_bins, void* m_out,
+                                     void* cm_m_out, const gvx_vec4_cview* bv, const gvx_vec3_cview* beta,
+                                     const gvx_vec4_view* bout, int64_t nb, gvx_stream_t stream) {
+  if (!valid_dtype(dtype) || !valid_coords(coords) || n < 0 || nb < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
+  const size_t es = dsize(dtype);
+  if (n > 0 && (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !lab_bins || !aligned(lab_bins, 8) || !cm_bins ||
+                !aligned(cm_bins, 8)))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if ((m_out && !aligned(m_out, es)) || (cm_m_out && !aligned(cm_m_out, es))) return GVX_ERR_INVALID_ARGUMENT;
+  if (nb > 0 && (!view_ok<4>(bv, es) || !view_ok<3>(beta, es) || !out_view_ok(bout, es)))
+    return GVX_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  // f64 only: the f32 pair pass is issue-bound and boost warps beside it made the step slower
+  // (1.46 vs 1.39 ms at 1e8); f32 takes the two calls.
+  const bool fast = dtype == GVX_F64 && n >= (int64_t(1) << 20) && nb >= (int64_t(1) << 20) &&
+                    coords == GVX_PTETAPHIM && tma_enabled() &&
+                    classify(v1, es) == L_AOS && classify(v2, es) == L_AOS && aos4(bv, es) && aos3(beta, es) &&
+                    aos4(bout, es) && getenv("GVX_NO_STEP_KERNEL") == nullptr;
+  if (fast) {
+    const HistParams hp = make_hist_params(lo, hi, nbins);
+    const double* pv = (const double*)bv->c[0];
+    const double* pb = (const double*)beta->c[0];
+    double* po = (double*)bout->c[0];
+    gvx_status st;
+    const char* cfg = getenv("GVX_STEP_CFG");
+    const int c = cfg ? atoi(cfg) : 2;  // 2: 18 pair warps + 6 boost warps (tools/step_probe.py: 2.62 vs 2.67-2.77 ms)
+    if (c == 1)
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 512, 3, 8>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 0)
+      st = launch_step<double, PairTma<double, 1280, 2, 20, 1>, BoostRing<double, 256, 4, 4>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else
+      st = launch_step<double, PairTma<double, 1152, 2, 18, 1>, BoostRing<double, 384, 3, 6>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    if (st != GVX_ERR_UNSUPPORTED) return st;
+  }
+  // any other shape: the two calls it fuses (same bits)
+  gvx_status st = n > 0 ? gvx_pair_histograms(dtype, coords, v1, v2, n, lo, hi, nbins, lab_bins, cm_bins, m_out,
+                                              cm_m_out, stream)
+                        : GVX_OK;
+  if (st != GVX_OK || nb == 0) return st;
+  return gvx_boost(dtype, bv, beta, bout, nb, stream);
 }
 
 gvx_status gvx_cm_costheta_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,

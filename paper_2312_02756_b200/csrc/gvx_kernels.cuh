@@ -1101,4 +1101,171 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
   }
 }
 
+// ============================================================================
+// The whole bench step in ONE persistent launch (k_step): the fused pair pass
+// (PM_BOTH on AoS PtEtaPhiM pairs) and the per-event boost of a second batch
+// (AoS vectors, AoS [N][3] velocities) share every SM. The pair pass is bound
+// by the FP64 pipe at ~5 TB/s and the boost by HBM, so running them in the same
+// CTA lets the memory system stream the boost while the FP64 pipe works on the
+// pairs. Warp 0, lane 0 feeds two TMA rings (pair tiles, boost tiles) without
+// blocking on either; warps 1..NCW consume pairs exactly as k_pair_tma does
+// (same arithmetic, same bits); warps NCW+1..NCW+NBW boost (boost_coef /
+// apply_boost as k_boost: same bits) and store with 256-bit STG.
+// ============================================================================
+template <typename T, int BT_, int BST_, int NBW_>
+struct BoostRing {
+  static constexpr int BT = BT_, BST = BST_, NBW = NBW_, NBT = NBW * 32;
+  static constexpr int EPB = BT / NBT;              // boost events per thread per stage
+  static constexpr int VB = BT * 4 * (int)sizeof(T);  // vector tile bytes
+  static constexpr int BB = BT * 3 * (int)sizeof(T);  // velocity tile bytes
+  static constexpr int STAGE_BYTES = VB + BB;
+  static constexpr int RING_BYTES = BST * STAGE_BYTES;
+  static_assert(BT % NBT == 0 && BB % 16 == 0 && VB % 16 == 0, "boost tile geometry");
+};
+
+template <typename T, typename CFG, typename BR>
+__global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
+    k_step(View4<T> v1, View4<T> v2, int64_t n, T* __restrict__ m_out, HistParams hp,
+           unsigned long long* __restrict__ bins, CosOut<T> co, const T* __restrict__ bv, const T* __restrict__ bb,
+           T* __restrict__ bout, int64_t nb) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* ring = reinterpret_cast<T*>(smem);
+  unsigned char* bring = smem + CFG::RING_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bring + BR::RING_BYTES);
+  uint64_t* empty = full + CFG::STAGES;
+  uint64_t* bfull = empty + CFG::STAGES;
+  uint64_t* bempty = bfull + BR::BST;
+  unsigned int* sh_hist = reinterpret_cast<unsigned int*>(bempty + BR::BST);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb2 = hp.nbins + 2;
+  const int nbt = nb2 + co.hc.nbins + 2;
+  unsigned int* sh_cos = sh_hist + nb2;
+  for (int b = threadIdx.x; b < nbt; b += blockDim.x) sh_hist[b] = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CFG::STAGES; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], CFG::NCW);
+    }
+    for (int s = 0; s < BR::BST; ++s) {
+      tma::mbar_init(&bfull[s], 1);
+      tma::mbar_init(&bempty[s], BR::NBW);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+
+  const int64_t ntiles = n / CFG::TILE, nbtiles = nb / BR::BT;
+  constexpr int TV = CFG::TILE * 4;
+  if (warp == 0) {
+    if (lane == 0) {  // producer of both rings; never blocks on one while the other can move
+      const uint64_t pol = tma::policy_evict_first();
+      int64_t t = blockIdx.x, tb = blockIdx.x;
+      int s = 0, it = 0, bs = 0, bit = 0;
+      uint32_t ph = 1, bph = 1;
+      while (t < ntiles || tb < nbtiles) {
+        bool moved = false;
+        if (t < ntiles && (it < CFG::STAGES || tma::mbar_try_wait(&empty[s], ph))) {
+          if (it >= CFG::STAGES) tma::fence_proxy_async_smem();
+          tma::mbar_arrive_expect_tx(&full[s], CFG::STAGE_BYTES);
+          T* dst = ring + (size_t)s * 2 * TV;
+          tma::bulk_g2s(dst, v1.c[0] + t * TV, CFG::HALF, &full[s], pol);
+          tma::bulk_g2s(dst + TV, v2.c[0] + t * TV, CFG::HALF, &full[s], pol);
+          ++it;
+          if (++s == CFG::STAGES) { s = 0; ph ^= 1u; }
+          t += gridDim.x;
+          moved = true;
+        }
+        if (tb < nbtiles && (bit < BR::BST || tma::mbar_try_wait(&bempty[bs], bph))) {
+          if (bit >= BR::BST) tma::fence_proxy_async_smem();
+          tma::mbar_arrive_expect_tx(&bfull[bs], BR::STAGE_BYTES);
+          unsigned char* dst = bring + (size_t)bs * BR::STAGE_BYTES;
+          tma::bulk_g2s(dst, bv + tb * BR::BT * 4, BR::VB, &bfull[bs], pol);
+          tma::bulk_g2s(dst + BR::VB, bb + tb * BR::BT * 3, BR::BB, &bfull[bs], pol);
+          ++bit;
+          if (++bs == BR::BST) { bs = 0; bph ^= 1u; }
+          tb += gridDim.x;
+          moved = true;
+        }
+        if (!moved) __nanosleep(64);
+      }
+    }
+  } else if (warp <= CFG::NCW) {  // pair consumers (the k_pair_tma PM_BOTH loop)
+    const int ctid = threadIdx.x - 32;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      tma::mbar_wait(&full[s], ph);
+      const T* src = ring + (size_t)s * 2 * TV;
+      T a[CFG::EPT][4], b[CFG::EPT][4];
+#pragma unroll
+      for (int u = 0; u < CFG::EPT; ++u) {
+        const int e = u * CFG::NCT + ctid;
+        lds_vec(src, e, lane, a[u]);
+        lds_vec(src + TV, e, lane, b[u]);
+      }
+      tma::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[s]);
+      static_assert(CFG::EPT % 2 == 0, "two events per call");
+#pragma unroll
+      for (int u = 0; u < CFG::EPT; u += 2)
+        pair_consume_x2<C_PTETAPHIM, PM_BOTH>(a[u], b[u], a[u + 1], b[u + 1], t * CFG::TILE + u * CFG::NCT + ctid,
+                                             t * CFG::TILE + (u + 1) * CFG::NCT + ctid, m_out, sh_hist, hp,
+                                             View4o<T>{}, sh_cos, co);
+      if (++s == CFG::STAGES) { s = 0; ph ^= 1u; }
+    }
+    if (blockIdx.x == gridDim.x - 1) {
+      for (int64_t i = ntiles * CFG::TILE + ctid; i < n; i += CFG::NCT) {
+        T a[4], b[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { a[c] = v1.c[0][4 * i + c]; b[c] = v2.c[0][4 * i + c]; }
+        pair_consume<T, C_PTETAPHIM, PM_BOTH, false>(a, b, i, m_out, sh_hist, hp, View4o<T>{}, sh_cos, co);
+      }
+    }
+  } else {  // boost warps
+    const int btid = threadIdx.x - 32 * (CFG::NCW + 1);
+    View4o<T> o;
+    o.c[0] = bout; o.c[1] = bout + 1; o.c[2] = bout + 2; o.c[3] = bout + 3; o.s = 4;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t tb = blockIdx.x; tb < nbtiles; tb += gridDim.x) {
+      tma::mbar_wait(&bfull[s], ph);
+      const T* sv = reinterpret_cast<const T*>(bring + (size_t)s * BR::STAGE_BYTES);
+      const T* sb = reinterpret_cast<const T*>(bring + (size_t)s * BR::STAGE_BYTES + BR::VB);
+      T x[BR::EPB][4], bx[BR::EPB], by[BR::EPB], bz[BR::EPB];
+#pragma unroll
+      for (int u = 0; u < BR::EPB; ++u) {
+        const int e = u * BR::NBT + btid;
+        lds_vec(sv, e, lane, x[u]);
+        bx[u] = sb[3 * e];
+        by[u] = sb[3 * e + 1];
+        bz[u] = sb[3 * e + 2];
+      }
+      tma::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&bempty[s]);
+#pragma unroll
+      for (int u = 0; u < BR::EPB; ++u) {
+        const int64_t i = tb * BR::BT + u * BR::NBT + btid;
+        boost_store<T, true>(o, i, apply_boost(boost_coef(bx[u], by[u], bz[u]), V4<T>{x[u][0], x[u][1], x[u][2], x[u][3]}));
+      }
+      if (++s == BR::BST) { s = 0; ph ^= 1u; }
+    }
+    if (blockIdx.x == gridDim.x - 1) {  // ragged boost tail
+      for (int64_t i = nbtiles * BR::BT + btid; i < nb; i += BR::NBT) {
+        V4<T> x{bv[4 * i], bv[4 * i + 1], bv[4 * i + 2], bv[4 * i + 3]};
+        boost_store<T, true>(o, i, apply_boost(boost_coef(bb[3 * i], bb[3 * i + 1], bb[3 * i + 2]), x));
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbt; b += blockDim.x) {
+    unsigned int c = sh_hist[b];
+    if (c) {
+      if (b < nb2) hist_flush(bins, hp, b, c);
+      else atomicAdd(&co.bins[b - nb2], (unsigned long long)c);
+    }
+  }
+}
+
 }  // namespace gvx

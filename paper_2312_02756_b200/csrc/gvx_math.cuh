@@ -407,7 +407,9 @@ template <typename T>
 __device__ __forceinline__ BoostCoef<T> boost_coef(T bx, T by, T bz) {
   BoostCoef<T> k;
   k.bx = bx; k.by = by; k.bz = bz;
-  T b2 = bx * bx + by * by + bz * bz;
+  // explicit fma order: the same bits in every kernel that inlines this (the
+  // one-launch step must match the standalone boost bit for bit)
+  T b2 = fma(bz, bz, fma(by, by, bx * bx));
   k.ok = b2 < T(1);
   T g = T(1) / ieee_sqrt(T(1) - b2);
   k.g = g;
@@ -452,11 +454,12 @@ __device__ __forceinline__ V4<T> apply_boost(const BoostCoef<T>& k, const V4<T>&
     o.x = o.y = o.z = o.t = nan;
     return o;
   }
-  T bp = Y0 ? k.bx * v.x + k.bz * v.z : k.bx * v.x + k.by * v.y + k.bz * v.z;
-  T f = k.bg * bp + k.g * v.t;
-  o.x = v.x + f * k.bx;
-  o.y = Y0 ? f * k.by : v.y + f * k.by;
-  o.z = v.z + f * k.bz;
+  // explicit fma order (context-independent bits, see boost_coef)
+  T bp = Y0 ? fma(k.bz, v.z, k.bx * v.x) : fma(k.bz, v.z, fma(k.by, v.y, k.bx * v.x));
+  T f = fma(k.bg, bp, k.g * v.t);
+  o.x = fma(f, k.bx, v.x);
+  o.y = Y0 ? f * k.by : fma(f, k.by, v.y);
+  o.z = fma(f, k.bz, v.z);
   o.t = k.g * (v.t + bp);
   return o;
 }

@@ -1163,3 +1163,28 @@ def test_pair_histograms_other_branches(gvx, dt, case):
         assert torch.equal(lab, lab0) and torch.equal(cmb, lab0)
     else:
         assert int((lab - lab0).sum()) == n and int((cmb - lab0).sum()) == n
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("sizes", [((1 << 20) + 37, (1 << 20) + 11), ((1 << 21) + 5, (1 << 20) + 3),
+                                   ((1 << 20) + 1, (1 << 22) + 7), (1000, 5000)])
+def test_pair_histograms_boost_one_launch(gvx, dt, sizes):
+    """gvx_pair_histograms_boost (the step in one launch: pair ring + boost ring on every SM) ==
+    gvx_pair_histograms + gvx_boost bit for bit — bins, lab and CM masses, boosted vectors —
+    with ragged pair and boost tails, unequal batch sizes (either one finishing first) and a
+    small batch (the two-call fallback)."""
+    n, nb = sizes
+    v1, v2 = mixed_inputs(n, dt, seed=21)
+    n = v1.shape[0]
+    t1, t2 = dev(v1), dev(v2)
+    x, beta = synth.boost_inputs(np.arange(nb), dtype=dt, seed=8)
+    tx, tb = dev(x), dev(beta)
+    m, mc, m_ref, mc_ref = (torch.empty(n, dtype=TDT[dt], device="cuda") for _ in range(4))
+    lab, cmb, out = gvx.pair_histograms_boost(t1, t2, tx, tb, m_out=m, cm_m_out=mc)
+    lab_ref, cmb_ref = gvx.pair_histograms(t1, t2, m_out=m_ref, cm_m_out=mc_ref)
+    out_ref = gvx.boost(tx, tb)
+    assert torch.equal(lab, lab_ref) and torch.equal(cmb, cmb_ref)
+    assert int(lab.sum()) == n and int(cmb.sum()) == n
+    assert np.array_equal(host(m), host(m_ref), equal_nan=True)
+    assert np.array_equal(host(mc), host(mc_ref), equal_nan=True)
+    assert np.array_equal(host(out), host(out_ref), equal_nan=True)

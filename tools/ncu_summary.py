@@ -35,6 +35,8 @@ METRICS = [
 def kernel_key(name: str):
     if "k_boost_inputs" in name or "k_muon_pairs" in name or "k_jagged" in name:
         return None  # the input generator (synth/), not a hot-path kernel
+    if "k_step" in name:
+        return "step"
     if "k_boost" in name:
         return "boost"
     cm = None
@@ -57,7 +59,7 @@ def main():
     n = int(float(sys.argv[4])) if len(sys.argv) > 4 else 100_000_000
     es = 8 if dtype == "f64" else 4
     algo = {"invariant_mass": 9 * es, "boost": 11 * es, "mass_histogram": 8 * es, "mass_histogram_cm": 8 * es,
-            "cm_costheta_hist": 8 * es, "pairs": 9 * es}
+            "cm_costheta_hist": 8 * es, "pairs": 9 * es, "step": 20 * es}
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, units = rows[0], rows[1]

@@ -36,5 +36,6 @@ for _ in range(a.reps):
     gvx.mass_histogram(v1, v2, bins=bins, cm=True)
     gvx.cm_costheta_histogram(v1, v2)
     gvx.pair_histograms(v1, v2, m_out=m)
+    gvx.pair_histograms_boost(v1, v2, bv, bb, m_out=m, out=out)
 torch.cuda.synchronize()
 print("prof_step done")

@@ -16,6 +16,6 @@ if [ "$1" = bench ]; then
   python bench.py --sweep --sweep-out gpurun_out/nsweep_cfg2.jsonl > gpurun_out/sweep.log 2>> gpurun_out/refresh.err
 elif [ "$1" = ncu ]; then
   dt=${2:-f64}
-  ncu --set full --import-source on --clock-control none -k regex:"k_pair_tma|k_boost|k_invariant_mass|k_mass_histogram|k_cm_costheta" \
+  ncu --set full --import-source on --clock-control none -k regex:"k_step|k_pair_tma|k_boost|k_invariant_mass|k_mass_histogram|k_cm_costheta" \
       -f -o gpurun_out/prof_$dt python tools/prof_step.py --dtype $dt > gpurun_out/prof_$dt.log 2>&1
 fi
