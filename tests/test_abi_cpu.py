@@ -127,6 +127,33 @@ def test_pair_histograms_validation(gvx):
     assert call(n=0, ax=(1.0, 1.0, 10)) == 1              # ... but a bad axis is still an error
 
 
+def test_pair_histograms_boost_validation(gvx):
+    """gvx_pair_histograms_boost (ABI v6) validates the axis, the pair and the boost arguments
+    synchronously; empty batches are OK with nothing launched."""
+    L = gvx.lib
+    by = ctypes.byref
+    a, b, v = _view(), _view(), _view()
+    beta = gvx.Vec3CView()
+    beta.c[0], beta.c[1], beta.c[2], beta.stride = 0x9000, 0x9008, 0x9010, 3
+    out = gvx.Vec4View()
+    for k in range(4):
+        out.c[k] = 0xA000 + 8 * k
+    out.stride = 4
+    F = L.gvx_pair_histograms_boost
+
+    def call(n=4, nb=4, ax=(0.25, 300.0, 1000), lb=0x4000, cb=0x5000, dt=gvx.GVX_F64, coords=0, bo=out):
+        return F(dt, coords, by(a), by(b), n, ax[0], ax[1], ax[2], lb, cb, None, None, by(v), by(beta), by(bo), nb,
+                 None)
+
+    assert call(ax=(1.0, 1.0, 10)) == 1 and call(ax=(0.0, 1.0, 0)) == 1
+    assert call(lb=None) == 1 and call(cb=0x5004) == 1
+    assert call(n=-1) == 1 and call(nb=-1) == 1 and call(dt=7) == 1 and call(coords=9) == 1
+    bad = gvx.Vec4View()
+    bad.c[0], bad.stride = 0xA001, 4
+    assert call(bo=bad) == 1                              # misaligned boost output
+    assert call(n=0, nb=0, lb=None, cb=None) == 0         # both batches empty: nothing launched
+
+
 def test_mass_histogram_peers_validation(gvx):
     """The fused-reduction entry point (ABI v4) checks its sink arguments synchronously."""
     L = gvx.lib
