@@ -1164,7 +1164,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
       uint32_t ph = 1, bph = 1;
       while (t < ntiles || tb < nbtiles) {
         bool moved = false;
-        if (t < ntiles && (it < CFG::STAGES || tma::mbar_try_wait(&empty[s], ph))) {
+        if (t < ntiles && (it < CFG::STAGES || tma::mbar_try_wait_hint(&empty[s], ph, 64u))) {
           if (it >= CFG::STAGES) tma::fence_proxy_async_smem();
           tma::mbar_arrive_expect_tx(&full[s], CFG::STAGE_BYTES);
           T* dst = ring + (size_t)s * 2 * TV;
@@ -1175,7 +1175,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
           t += gridDim.x;
           moved = true;
         }
-        if (tb < nbtiles && (bit < BR::BST || tma::mbar_try_wait(&bempty[bs], bph))) {
+        if (tb < nbtiles && (bit < BR::BST || tma::mbar_try_wait_hint(&bempty[bs], bph, 64u))) {
           if (bit >= BR::BST) tma::fence_proxy_async_smem();
           tma::mbar_arrive_expect_tx(&bfull[bs], BR::STAGE_BYTES);
           unsigned char* dst = bring + (size_t)bs * BR::STAGE_BYTES;
@@ -1186,7 +1186,6 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
           tb += gridDim.x;
           moved = true;
         }
-        if (!moved) __nanosleep(64);
       }
     }
   } else if (warp <= CFG::NCW) {  // pair consumers (the k_pair_tma PM_BOTH loop)

@@ -1188,3 +1188,23 @@ def test_pair_histograms_boost_one_launch(gvx, dt, sizes):
     assert np.array_equal(host(m), host(m_ref), equal_nan=True)
     assert np.array_equal(host(mc), host(mc_ref), equal_nan=True)
     assert np.array_equal(host(out), host(out_ref), equal_nan=True)
+
+
+def test_one_launch_step_repeat_bitwise(gvx):
+    """Ring-reuse stress for k_step (the check that caught the missing proxy fence in the pair
+    ring): L2-sized batches (2^20 pairs, 2^20 boosts: each CTA cycles both rings many times with
+    L2-resident refills) run 40 times; every run equals the two-call result bit for bit."""
+    import synth.device as sd
+    n = nb = 1 << 20
+    v1, v2 = sd.muon_pairs(n, dtype=torch.float64)
+    bv, bb = sd.boost_inputs(nb, dtype=torch.float64)
+    m_ref = torch.empty(n, dtype=torch.float64, device="cuda")
+    lab_ref, cm_ref = gvx.pair_histograms(v1, v2, m_out=m_ref)
+    out_ref = gvx.boost(bv, bb)
+    m = torch.empty_like(m_ref)
+    out = torch.empty_like(out_ref)
+    for _ in range(40):
+        lab, cmb, _o = gvx.pair_histograms_boost(v1, v2, bv, bb, m_out=m, out=out)
+        assert torch.equal(lab, lab_ref) and torch.equal(cmb, cm_ref)
+        assert torch.equal(m.view(torch.int64), m_ref.view(torch.int64))
+        assert torch.equal(out.view(torch.int64), out_ref.view(torch.int64))
