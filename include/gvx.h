@@ -15,9 +15,11 @@
  *   device) launch-configuration cache (SM count, occupancy, shared-memory
  *   opt-in), filled on first use under a mutex — so every entry point may be
  *   called from several host threads and captured into a CUDA graph after one
- *   warm-up call. Environment: GVX_DISABLE_TMA=1 / GVX_FORCE_TMA=1 pick the
- *   register (LDG) or shared-memory-ring (TMA) kernels for A/B runs; results
- *   are identical either way. Outputs are
+ *   warm-up call. Environment (read once per process): GVX_DISABLE_TMA=1 /
+ *   GVX_FORCE_TMA=1 pick the register (LDG) or shared-memory-ring (TMA)
+ *   kernels, GVX_NO_STEP_KERNEL=1 runs gvx_pair_histograms_boost as its two
+ *   calls, GVX_DIMUON_IMPL=tma|ldg picks the streaming dimuon kernels — all for
+ *   A/B runs; results are identical either way. Outputs are
  *   caller-allocated, as in the paper's kernel signature
  *   `(LVector *v1, LVector *v2, Scalar *m, size_t N)`.
  * Asynchrony. Device entry points enqueue on `stream` and return without a
@@ -279,6 +281,11 @@ gvx_status gvx_dimuon_histogram(gvx_dtype dtype, const gvx_vec4_cview *muons, co
  *   gvx_host_pairs: n AoS pairs (h_v1, h_v2, layout by `coords`); any of
  *            h_m_out (n masses), h_bins / h_bins_cm (nbins+2 uint64 each,
  *            OVERWRITTEN with this batch's lab / CM histogram) may be NULL.
+ *            Arguments are validated before anything is enqueued, with the
+ *            device entries' rules (coords, 1 <= nbins <= 2^28, finite
+ *            lo < hi when a histogram is requested) -> INVALID_ARGUMENT.
+ *   Consecutive calls on one pipeline are ordered (each waits for the whole
+ *   previous call, whatever caller stream either used).
  *   gvx_host_boost: n PxPyPzE vectors h_v, n betas h_beta (AoS [n][3]),
  *            h_out (n vectors).
  */

@@ -169,6 +169,12 @@ bool force_tma() {
   }();
   return force;
 }
+// GVX_NO_STEP_KERNEL=1: gvx_pair_histograms_boost runs as its two calls (A/B runs;
+// read once, like the other switches).
+bool step_kernel_enabled() {
+  static const bool on = [] { return getenv("GVX_NO_STEP_KERNEL") == nullptr; }();
+  return on;
+}
 template <typename T, int MODE>
 bool tma_preferred() {
   return force_tma() || sizeof(T) == 8 || MODE != PM_MASS;
@@ -844,18 +850,22 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
   cudaStream_t s = (cudaStream_t)stream;
   // f64 only: the f32 pair pass is issue-bound and boost warps beside it made the step slower
   // (1.46 vs 1.39 ms at 1e8); f32 takes the two calls.
+  // bout: the boost warps store with 256-bit STG (st.global.v4.f64), which needs 32-byte rows
   const bool fast = dtype == GVX_F64 && n >= (int64_t(1) << 20) && nb >= (int64_t(1) << 20) &&
-                    coords == GVX_PTETAPHIM && tma_enabled() &&
+                    coords == GVX_PTETAPHIM && tma_enabled() && step_kernel_enabled() &&
                     classify(v1, es) == L_AOS && classify(v2, es) == L_AOS && aos4(bv, es) && aos3(beta, es) &&
-                    aos4(bout, es) && getenv("GVX_NO_STEP_KERNEL") == nullptr;
+                    aos4(bout, es) && aligned(bout->c[0], 4 * es);
   if (fast) {
     const HistParams hp = make_hist_params(lo, hi, nbins);
     const double* pv = (const double*)bv->c[0];
     const double* pb = (const double*)beta->c[0];
     double* po = (double*)bout->c[0];
     gvx_status st;
-    const char* cfg = getenv("GVX_STEP_CFG");
-    const int c = cfg ? atoi(cfg) : 2;  // 2: 18 pair warps + 6 boost warps (tools/step_probe.py: 2.62 vs 2.67-2.77 ms)
+#ifdef GVX_TUNE
+    const int c = tune_env("GVX_STEP_CFG") ? tune_env("GVX_STEP_CFG") : 2;
+#else
+    const int c = 2;  // 18 pair warps + 6 boost warps (tools/step_probe.py: 2.62 vs 2.67-2.77 ms)
+#endif
     if (c == 1)
       st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 512, 3, 8>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);

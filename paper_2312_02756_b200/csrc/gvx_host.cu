@@ -8,6 +8,7 @@
 // kernels are the device entry points of gvx_api.cu, called on the compute
 // stream — this file adds no arithmetic.
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -83,10 +84,14 @@ gvx_vec4_view aos_oview(void* base, size_t es) {
   return v;
 }
 
-// Fork the pipeline's streams off the caller's stream (and after the previous
-// call on this pipeline, whatever stream that used: staging slots are reused).
+// Fork the pipeline's streams off the caller's stream, and after the whole
+// previous call on this pipeline (whatever stream that used): the staging slots
+// and d_bins are reused, so none of the three streams may start before that
+// call's last D2H (ev_done, recorded on s_out by join) has completed.
 void fork(gvx_host_pipeline* p, cudaStream_t caller) {
   cudaStreamWaitEvent(p->s_in, p->ev_done, 0);
+  cudaStreamWaitEvent(p->s_cmp, p->ev_done, 0);
+  cudaStreamWaitEvent(p->s_out, p->ev_done, 0);
   cudaEventRecord(p->ev_start, caller);
   cudaStreamWaitEvent(p->s_in, p->ev_start, 0);
   cudaStreamWaitEvent(p->s_cmp, p->ev_start, 0);
@@ -156,9 +161,13 @@ gvx_status gvx_host_pipeline_destroy(gvx_host_pipeline* p) {
 gvx_status gvx_host_pairs(gvx_host_pipeline* p, gvx_coords coords, const void* h_v1, const void* h_v2, int64_t n,
                           double lo, double hi, int32_t nbins, void* h_m_out, unsigned long long* h_bins,
                           unsigned long long* h_bins_cm, gvx_stream_t stream) {
+  // validated synchronously, before anything is enqueued (the device entries' rules)
   if (!p || n < 0 || (n > 0 && (!h_v1 || !h_v2))) return GVX_ERR_INVALID_ARGUMENT;
+  if (coords != GVX_PTETAPHIM && coords != GVX_PXPYPZE && coords != GVX_PXPYPZM && coords != GVX_PTETAPHIE)
+    return GVX_ERR_INVALID_ARGUMENT;
   const bool hist = h_bins || h_bins_cm;
-  if (hist && (nbins < 1 || nbins > (1 << 24) || !(lo < hi))) return GVX_ERR_INVALID_ARGUMENT;
+  if (hist && (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)))
+    return GVX_ERR_INVALID_ARGUMENT;
   DeviceGuard guard(p->device);
   cudaStream_t caller = (cudaStream_t)stream;
   const size_t es = p->es, vb = 4 * es;

@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(256) k_dimuon_histogram(View4<T> mu, const int
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) sel[u] = two[u] && __ldg(q + o[u]) * __ldg(q + o[u] + 1) < 0;
+    for (int u = 0; u < U; ++u) sel[u] = two[u] && (int64_t)__ldg(q + o[u]) * (int64_t)__ldg(q + o[u] + 1) < 0;
     T a[U][4], b[U][4];
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
         const int el = u * CFG::NCT + ctid;
         const int64_t o = so[el], kk = so[el + 1] - o;
         const int32_t* pq = qov ? q + o : sq + (o - q0);
-        sel[u] = kk == 2 && pq[0] * pq[1] < 0;
+        sel[u] = kk == 2 && (int64_t)pq[0] * (int64_t)pq[1] < 0;
         if (sel[u]) {
           const T* pa = ov ? mu + 4 * o : sm + 4 * (o - m0);
 #pragma unroll
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
       for (int64_t e = ntiles * CFG::ET + ctid; e < n_events; e += CFG::NCT) {
         const int64_t o = __ldg(offsets + e), kk = __ldg(offsets + e + 1) - o;
         T M = T(NAN);
-        if (kk == 2 && __ldg(q + o) * __ldg(q + o + 1) < 0) {
+        if (kk == 2 && (int64_t)__ldg(q + o) * (int64_t)__ldg(q + o + 1) < 0) {
           T a[4], b[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) { a[c] = mu[4 * o + c]; b[c] = mu[4 * o + 4 + c]; }
@@ -1162,8 +1162,9 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
       int64_t t = blockIdx.x, tb = blockIdx.x;
       int s = 0, it = 0, bs = 0, bit = 0;
       uint32_t ph = 1, bph = 1;
+      // each mbarrier poll is a try_wait with a 64 ns suspend-time hint, so a producer
+      // waiting on both rings sleeps in the barrier unit instead of spinning on issue slots
       while (t < ntiles || tb < nbtiles) {
-        bool moved = false;
         if (t < ntiles && (it < CFG::STAGES || tma::mbar_try_wait_hint(&empty[s], ph, 64u))) {
           if (it >= CFG::STAGES) tma::fence_proxy_async_smem();
           tma::mbar_arrive_expect_tx(&full[s], CFG::STAGE_BYTES);
@@ -1173,7 +1174,6 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
           ++it;
           if (++s == CFG::STAGES) { s = 0; ph ^= 1u; }
           t += gridDim.x;
-          moved = true;
         }
         if (tb < nbtiles && (bit < BR::BST || tma::mbar_try_wait_hint(&bempty[bs], bph, 64u))) {
           if (bit >= BR::BST) tma::fence_proxy_async_smem();
@@ -1184,7 +1184,6 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
           ++bit;
           if (++bs == BR::BST) { bs = 0; bph ^= 1u; }
           tb += gridDim.x;
-          moved = true;
         }
       }
     }

@@ -672,3 +672,122 @@ def test_boost_high_beta_stress(O):
         t = truth_boost(v[i], beta[i])
         worst = max(worst, max(abs(float(out[i, k]) - float(t[k])) for k in range(4)) / float(S[i]))
     assert worst <= 1e-12, worst
+
+
+# --------------------------------------------------------------------------
+# The boost tolerance scale S = γ(E + |β||p|) (reading R5), pinned by closed forms
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_boost_scale_closed_forms(O, dt):
+    """S is the denominator of every boost parity check, so it is pinned to quantities
+    computed along the rapidity route, not by retyping its formula:
+    * a massless vector along β̂ has E' = γ(1 + |β|)E (the Doppler factor), and S = E' there;
+    * a particle at rest has E' = γm and S = γm;
+    * for physical vectors (|p| ≤ E) S bounds every row of |Λ|·|v| and is within 2× of the
+      largest row: max_r Σ_j |Λ_rj||v_j| ≤ S ≤ 2 max_r Σ_j |Λ_rj||v_j|."""
+    eps = float(np.finfo(dt).eps)
+    rng = np.random.default_rng(404)
+    for bmag in (0.1, 0.5, 0.9, 0.99):
+        for _ in range(6):
+            n = rng.normal(size=3)
+            n /= np.linalg.norm(n)
+            for E in (1.0, 37.5):
+                v = np.array([[E * n[0], E * n[1], E * n[2], E]], dt)
+                beta = np.array([bmag * n], dt)
+                _, s = O.boost(v, beta)
+                Ep = truth_boost(v[0], beta[0])[3]  # the boosted energy, rapidity route
+                g2 = 1 / (1 - bmag * bmag)
+                assert abs(mp.mpf(float(s[0])) - Ep) <= 16 * eps * g2 * Ep, (bmag, E, float(s[0]), float(Ep))
+                # and the closed form γ(1+β)E = E·sqrt((1+β)/(1−β)) itself
+                assert float(Ep) == pytest.approx(E * math.sqrt((1 + bmag) / (1 - bmag)), rel=64 * eps * g2)
+            # rest particle of mass m: S = γm = E'
+            m = 0.1056583755 if dt == np.float64 else 5.0
+            v = np.array([[0.0, 0.0, 0.0, m]], dt)
+            beta = np.array([bmag * n], dt)
+            _, s = O.boost(v, beta)
+            Ep = truth_boost(v[0], beta[0])[3]
+            assert abs(mp.mpf(float(s[0])) - Ep) <= 16 * eps * g2 * Ep
+    # random physical events: S bounds |Λ|·|v| row by row, tightly (40-digit Λ from β)
+    v, beta = synth.boost_inputs(np.arange(300), seed=13, dtype=dt)
+    _, s = O.boost(v, beta)
+    for i in range(len(v)):
+        bx, by, bz = (mp.mpf(float(x)) for x in beta[i])
+        b2 = bx * bx + by * by + bz * bz
+        g = 1 / mp.sqrt(1 - b2)
+        bg = g * g / (1 + g)
+        b = [bx, by, bz]
+        L = [[(1 if r == c else 0) + bg * b[r] * b[c] for c in range(3)] + [g * b[r]] for r in range(3)]
+        L.append([g * bx, g * by, g * bz, g])
+        av = [abs(mp.mpf(float(x))) for x in v[i]]
+        rows = max(sum(abs(L[r][c]) * av[c] for c in range(4)) for r in range(4))
+        S = mp.mpf(float(s[i]))
+        assert rows * (1 - 64 * eps) <= S <= 2 * rows * (1 + 64 * eps), (i, float(S), float(rows))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_ptetaphim_energy_clamp(O, dt):
+    """Reading R2 (SPEC.md:81 is silent on m·|m| + pt² + pz² < 0): E² is clamped to 0, so a
+    spacelike vector whose |m| exceeds its |p| has E = 0 and, alone, mass −|p|:
+    (pt=1, η=0, φ=0, m=−5): E² = −24 → E = 0, M² = −1, M = −1;
+    (3, 0, 0, −4): E² = −7 → E = 0, M = −3; (3, 0, 0, −3): E² = 0 → E = 0, M = −3.
+    (√|E²| instead of the clamp would give E = √24 and M = +√23.)"""
+    z = np.zeros((1, 4), dt)
+    for v, M in (((1.0, 0.0, 0.0, -5.0), -1.0), ((3.0, 0.0, 0.0, -4.0), -3.0), ((3.0, 0.0, 0.0, -3.0), -3.0),
+                 ((2.0, 0.0, 1.0, -7.5), -2.0)):
+        m, e = O.invariant_mass(np.array([v], dt), z)
+        # (φ = 1: cos² + sin² is 1 only to a few ulp)
+        assert e[0] == 0.0 and m[0] == pytest.approx(M, rel=4 * np.finfo(dt).eps), (v, float(e[0]), float(m[0]))
+    # a clamped vector in a pair: E_lab = E of the other vector only; M² = E2² − |p1 + p2|²
+    a = np.array([[1.0, 0.0, 0.0, -5.0]], dt)   # p = (1, 0, 0), E = 0
+    b = np.array([[4.0, 0.0, 0.0, 3.0]], dt)    # p = (4, 0, 0), E = 5
+    m, e = O.invariant_mass(a, b)
+    assert e[0] == 5.0 and m[0] == 0.0         # M² = 25 − 25
+    # the same clamp on the CM path: the pair (a, b) is lightlike, E = 5 > 0, β = −1 → NaN (R11)
+    mc, _ = O.cm_mass(a, b)
+    assert np.isnan(mc[0])
+
+
+def test_boost_unit_speed_is_a_domain_error(O):
+    """|β| ≥ 1 → domain error — |β| = 1 exactly included (pre: b² < 1)."""
+    for b in ((0.0, 0.0, 1.0), (-1.0, 0.0, 0.0), (0.0, 1.0, 0.0)):
+        for dt in (np.float64, np.float32):
+            with pytest.raises(O.DomainError):
+                O.boost_uniform(np.ones((2, 4), dt), *b)
+
+
+def test_cm_conversion_components_spec_example(O):
+    """The Cartesian components of the conversion, seen through the CM boost (a pair's mass alone
+    only sees cos(φ1 − φ2), which a px <-> py swap leaves unchanged): SPEC.md:88's vector
+    a = PtEtaPhiM(10, 1.2, 0.5, 0.105) and SPEC.md:87's rest vector b = (0, 0, 0, 5). In the CM
+    frame b' is the rest particle boosted by β_cm = −p_a/(E_a + 5), so its momentum is
+    5γβ_cm = −5γ p_a/(E_a + 5) with p_a = (10 cos 0.5, 10 sin 0.5, 10 sinh 1.2), at 40 digits."""
+    a = np.array([[10.0, 1.2, 0.5, 0.105]])
+    b = np.array([[0.0, 0.0, 0.0, 5.0]])
+    m, _, bo = O.cm_mass(a, b, want_boosted=True)
+    p = [10 * mp.cos(mp.mpf(0.5)), 10 * mp.sin(mp.mpf(0.5)), 10 * mp.sinh(mp.mpf(1.2))]
+    Ea = mp.sqrt(mp.mpf(0.105) ** 2 + 100 * mp.cosh(mp.mpf(1.2)) ** 2)
+    E = Ea + 5
+    beta = [-x / E for x in p]
+    g = 1 / mp.sqrt(1 - sum(x * x for x in beta))
+    for k in range(3):
+        want = 5 * g * beta[k]
+        assert abs(bo[0, 4 + k] - want) <= 1e-14 * E, (k, bo[0, 4 + k], float(want))
+        assert abs(bo[0, k] + want) <= 1e-14 * E  # p'_a = −p'_b in the CM frame
+    assert abs(bo[0, 7] - 5 * g) <= 1e-14 * E
+    assert float(p[0]) == pytest.approx(8.7758256189037271612, rel=1e-16)   # S:88 as printed
+    assert float(p[1]) == pytest.approx(4.7942553860420300027, rel=1e-16)
+
+
+def test_cm_negative_energy_pair_has_no_rest_frame(O):
+    """Reading R11: β_cm = −P/E needs E > 0. A pair with negative total energy and P = 0 has
+    β_cm = 0 (|β| < 1) but no centre-of-mass frame: its CM mass is NaN (→ overflow bin)."""
+    a = np.array([[0.0, 0.0, 0.0, -5.0]])
+    b = np.array([[0.0, 0.0, 0.0, -3.0]])
+    m, _ = O.cm_mass(a, b, coords="pxpypze")
+    assert np.isnan(m[0])
+    bins, _ = O.mass_histogram(a, b, 0.25, 300.0, 1000, cm=True, coords="pxpypze")
+    assert bins[1001] == 1
+    # the lab mass of the same pair is defined: E² − p² = 64 → 8
+    ml, _ = O.invariant_mass(a, b, coords="pxpypze")
+    assert ml[0] == 8.0

@@ -19,7 +19,7 @@ METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
     ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU pipe %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
@@ -78,6 +78,8 @@ def main():
             continue
         vals = []
         for m, _ in METRICS:
+            if m not in h and m.startswith("gpu__dram_throughput") and "dram__throughput.avg.pct_of_peak_sustained_elapsed" in h:
+                m = "dram__throughput.avg.pct_of_peak_sustained_elapsed"  # older ncu name
             if m in h:
                 i = h.index(m)
                 vals.append(f"{r[i]} {units[i]}".strip())
