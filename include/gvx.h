@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define GVX_ABI_VERSION 6
+#define GVX_ABI_VERSION 7
 
 typedef struct CUstream_st *gvx_stream_t; /* == cudaStream_t */
 
@@ -298,6 +298,44 @@ gvx_status gvx_host_pairs(gvx_host_pipeline *p, gvx_coords coords, const void *h
                           gvx_stream_t stream);
 gvx_status gvx_host_boost(gvx_host_pipeline *p, const void *h_v, const void *h_beta, int64_t n,
                           void *h_out, gvx_stream_t stream);
+
+/*
+ * Mixed-coordinate pairs (ABI v7). The paper's kernel takes
+ * "two particles expressed in any 4-dimensional coordinate system"
+ * and the result must not depend on the systems the operands
+ * come in. These four calls are the pair entry points above with
+ * one coordinate system per operand: v1's components are in coords1, v2's in
+ * coords2 (component orders as in the header's Views paragraph). Each vector
+ * is converted to PxPyPzE on its own (clamp R2), then the
+ * pair is summed and its mass taken, or boosted to its
+ * CM frame first (R11). With coords1 == coords2 each call IS the single-system
+ * call (same kernels, same bits); otherwise one grid-stride kernel (256-bit
+ * loads for 32-byte AoS rows) serves every mixed combination. Arguments,
+ * outputs, accuracy and errors as the single-system calls; an invalid coords1
+ * or coords2 -> GVX_ERR_INVALID_ARGUMENT. gvx_pair_histograms_boost_mixed
+ * runs the boost of (bv, beta) as gvx_boost after the pair pass when the
+ * systems differ.
+ */
+gvx_status gvx_invariant_mass_mixed(gvx_dtype dtype, gvx_coords coords1, gvx_coords coords2,
+                                    const gvx_vec4_cview *v1, const gvx_vec4_cview *v2, void *m_out,
+                                    int64_t n, gvx_stream_t stream);
+gvx_status gvx_mass_histogram_mixed(gvx_dtype dtype, gvx_coords coords1, gvx_coords coords2,
+                                    const gvx_vec4_cview *v1, const gvx_vec4_cview *v2, int64_t n,
+                                    double lo, double hi, int32_t nbins, unsigned long long *bins,
+                                    uint32_t flags, void *m_out, const gvx_vec4_view *boosted_out,
+                                    gvx_stream_t stream);
+gvx_status gvx_pair_histograms_mixed(gvx_dtype dtype, gvx_coords coords1, gvx_coords coords2,
+                                     const gvx_vec4_cview *v1, const gvx_vec4_cview *v2, int64_t n,
+                                     double lo, double hi, int32_t nbins, unsigned long long *lab_bins,
+                                     unsigned long long *cm_bins, void *m_out, void *cm_m_out,
+                                     gvx_stream_t stream);
+gvx_status gvx_pair_histograms_boost_mixed(gvx_dtype dtype, gvx_coords coords1, gvx_coords coords2,
+                                           const gvx_vec4_cview *v1, const gvx_vec4_cview *v2,
+                                           int64_t n, double lo, double hi, int32_t nbins,
+                                           unsigned long long *lab_bins, unsigned long long *cm_bins,
+                                           void *m_out, void *cm_m_out, const gvx_vec4_cview *bv,
+                                           const gvx_vec3_cview *beta, const gvx_vec4_view *bout,
+                                           int64_t nb, gvx_stream_t stream);
 
 /* Human-readable name of a status code (static storage). */
 const char *gvx_status_string(gvx_status status);

@@ -50,7 +50,7 @@ def _load():
         P = ctypes.c_void_p
         I64 = ctypes.c_int64
         for sfx, T in (("f32", ctypes.c_float), ("f64", ctypes.c_double)):
-            getattr(lib, f"gvx_ref_invariant_mass_{sfx}").argtypes = [ctypes.c_int, P, P, I64, P, P]
+            getattr(lib, f"gvx_ref_invariant_mass_{sfx}").argtypes = [ctypes.c_int, ctypes.c_int, P, P, I64, P, P]
             getattr(lib, f"gvx_ref_boost_{sfx}").argtypes = [P, P, I64, P, P]
             f = getattr(lib, f"gvx_ref_boost_uniform_{sfx}")
             f.argtypes = [P, T, T, T, I64, P]
@@ -58,12 +58,12 @@ def _load():
             f = getattr(lib, f"gvx_ref_lorentz_transform_{sfx}")
             f.argtypes = [P, P, I64, P]
             f.restype = ctypes.c_int
-            getattr(lib, f"gvx_ref_cm_mass_{sfx}").argtypes = [ctypes.c_int, P, P, I64, P, P, P]
+            getattr(lib, f"gvx_ref_cm_mass_{sfx}").argtypes = [ctypes.c_int, ctypes.c_int, P, P, I64, P, P, P]
             getattr(lib, f"gvx_ref_mass_histogram_{sfx}").argtypes = [
-                ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                ctypes.c_int, ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                 ctypes.c_int, P, P]
             getattr(lib, f"gvx_ref_cm_costheta_{sfx}").argtypes = [
-                ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P,
+                ctypes.c_int, ctypes.c_int, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P,
                 ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P]
             f = getattr(lib, f"gvx_ref_dimuon_histogram_{sfx}")
             f.argtypes = [P, P, P, I64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P]
@@ -97,9 +97,16 @@ def _ptr(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data) if a is not None else None
 
 
-def invariant_mass(v1, v2, coords: str = "ptetaphim"):
+def _c2(coords: str, coords2):
+    """(coords of v1, coords of v2): the pair functions take each operand's coordinate system
+    (PAPER.md:136 "two particles expressed in any 4-dimensional coordinate system")."""
+    return _COORDS[coords], _COORDS[coords2 if coords2 is not None else coords]
+
+
+def invariant_mass(v1, v2, coords: str = "ptetaphim", coords2=None):
     """InvariantMasses, PAPER.md:141-151 (Fig. 1): ``m[i] = (v1[i] + v2[i]).mass()``.
 
+    ``v1`` is in ``coords``, ``v2`` in ``coords2`` (default: the same system).
     Returns ``(M, E_lab)``, both of v1's dtype; ``E_lab = E1 + E2`` is the
     tolerance scale (reading R5).
     """
@@ -111,7 +118,7 @@ def invariant_mass(v1, v2, coords: str = "ptetaphim"):
     m = np.empty(n, v1.dtype)
     e = np.empty(n, v1.dtype)
     getattr(_load(), f"gvx_ref_invariant_mass_{_sfx(v1.dtype)}")(
-        _COORDS[coords], _ptr(v1), _ptr(v2), n, _ptr(m), _ptr(e))
+        *_c2(coords, coords2), _ptr(v1), _ptr(v2), n, _ptr(m), _ptr(e))
     return m, e
 
 
@@ -160,7 +167,7 @@ def lorentz_transform(v, L):
     return out
 
 
-def cm_mass(v1, v2, coords: str = "ptetaphim", want_boosted: bool = False):
+def cm_mass(v1, v2, coords: str = "ptetaphim", want_boosted: bool = False, coords2=None):
     """Boost each pair to its CM frame (β = −P/E), then the signed mass (reading R11).
 
     Returns ``(M_cm, E_lab[, boosted])``; boosted is [N, 8] (vector 1, vector 2).
@@ -174,12 +181,12 @@ def cm_mass(v1, v2, coords: str = "ptetaphim", want_boosted: bool = False):
     e = np.empty(n, v1.dtype)
     bo = np.empty((n, 8), v1.dtype) if want_boosted else None
     getattr(_load(), f"gvx_ref_cm_mass_{_sfx(v1.dtype)}")(
-        _COORDS[coords], _ptr(v1), _ptr(v2), n, _ptr(m), _ptr(e), _ptr(bo))
+        *_c2(coords, coords2), _ptr(v1), _ptr(v2), n, _ptr(m), _ptr(e), _ptr(bo))
     return (m, e, bo) if want_boosted else (m, e)
 
 
 def mass_histogram(v1, v2, lo: float, hi: float, nbins: int, cm: bool = False,
-                   coords: str = "ptetaphim", bins=None):
+                   coords: str = "ptetaphim", bins=None, coords2=None):
     """Fused mass histogram (north_star; reading R12). Returns ``(bins uint64[nbins+2], M)``.
 
     ``bins`` accumulates if given (the caller's zeroed array)."""
@@ -193,12 +200,12 @@ def mass_histogram(v1, v2, lo: float, hi: float, nbins: int, cm: bool = False,
     assert bins.dtype == np.uint64 and bins.shape == (nbins + 2,) and bins.flags.c_contiguous
     m = np.empty(n, v1.dtype)
     getattr(_load(), f"gvx_ref_mass_histogram_{_sfx(v1.dtype)}")(
-        _COORDS[coords], _ptr(v1), _ptr(v2), n, lo, hi, nbins, int(bool(cm)), _ptr(bins), _ptr(m))
+        *_c2(coords, coords2), _ptr(v1), _ptr(v2), n, lo, hi, nbins, int(bool(cm)), _ptr(bins), _ptr(m))
     return bins, m
 
 
 def cm_costheta(v1, v2, m_axis=(0.25, 300.0, 1000), c_axis=(-1.0, 1.0, 100),
-                coords: str = "ptetaphim", m_bins=None, c_bins=None):
+                coords: str = "ptetaphim", m_bins=None, c_bins=None, coords2=None):
     """CM decay angle (reading R22): cos θ* = p'1z/|p'1| of vector 1 after
     the CM boost of reading R11, with the CM mass and cos θ* histograms (reading R12).
     Returns ``(m_bins, c_bins, M_cm, cos_theta)``; bins accumulate if given."""
@@ -214,7 +221,7 @@ def cm_costheta(v1, v2, m_axis=(0.25, 300.0, 1000), c_axis=(-1.0, 1.0, 100),
     m = np.empty(n, v1.dtype)
     c = np.empty(n, v1.dtype)
     getattr(_load(), f"gvx_ref_cm_costheta_{_sfx(v1.dtype)}")(
-        _COORDS[coords], _ptr(v1), _ptr(v2), n, float(m_axis[0]), float(m_axis[1]), int(m_axis[2]),
+        *_c2(coords, coords2), _ptr(v1), _ptr(v2), n, float(m_axis[0]), float(m_axis[1]), int(m_axis[2]),
         _ptr(m_bins), float(c_axis[0]), float(c_axis[1]), int(c_axis[2]), _ptr(c_bins), _ptr(m), _ptr(c))
     return m_bins, c_bins, m, c
 

@@ -13,6 +13,8 @@ Names follow the paper ("InvariantMasses", "ApplyBoost"):
 * :func:`mass_histogram` — fused mass (+ optional CM boost) histogram
 * :func:`sharded_mass_histogram` — per-rank histogram + NCCL bin all-reduce
 
+Pair calls take ``coords2`` for mixed pairs (v2 in another system than v1; ABI v7).
+
 Vector arguments are CUDA tensors ``[N, 4]`` (AoS, any row stride — e.g. the
 ``[:, 0, :]`` view of interleaved ``[N, 2, 4]`` pairs) or a 4-sequence of
 ``[N]`` tensors sharing one stride (SoA). Components are (pt, eta, phi, m)
@@ -43,7 +45,7 @@ GVX_PXPYPZE = 1
 GVX_PXPYPZM = 2
 GVX_PTETAPHIE = 3
 GVX_HIST_BOOST_TO_CM = 0x1
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 # The default histogram of the north star: 1000 bins over the dimuon range
 # (reading R13).
@@ -116,6 +118,15 @@ def _load_lib():
                                               ctypes.c_double, ctypes.c_double, ctypes.c_int32, P,
                                               ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P, P]
     lib.gvx_cm_costheta_histogram.restype = st
+    # mixed-coordinate pairs (ABI v7): the calls above with (coords1, coords2)
+    lib.gvx_invariant_mass_mixed.argtypes = [st, st] + lib.gvx_invariant_mass.argtypes[1:]
+    lib.gvx_invariant_mass_mixed.restype = st
+    lib.gvx_mass_histogram_mixed.argtypes = [st, st] + lib.gvx_mass_histogram.argtypes[1:]
+    lib.gvx_mass_histogram_mixed.restype = st
+    lib.gvx_pair_histograms_mixed.argtypes = [st, st] + lib.gvx_pair_histograms.argtypes[1:]
+    lib.gvx_pair_histograms_mixed.restype = st
+    lib.gvx_pair_histograms_boost_mixed.argtypes = [st, st] + lib.gvx_pair_histograms_boost.argtypes[1:]
+    lib.gvx_pair_histograms_boost_mixed.restype = st
     lib.gvx_status_string.argtypes = [st]
     lib.gvx_status_string.restype = ctypes.c_char_p
     lib.gvx_last_cuda_error_string.argtypes = []
@@ -156,6 +167,13 @@ def _coords_code(coords: str) -> int:
                 "ptetaphie": GVX_PTETAPHIE}[coords]
     except KeyError:
         raise ValueError(f"coords must be one of ptetaphim, pxpypze, pxpypzm, ptetaphie; got {coords!r}") from None
+
+
+def _coords_args(coords: str, coords2: Optional[str]):
+    """-> (mixed, codes): the single-system call's (coords,) or the mixed call's (coords1, coords2)."""
+    if coords2 is None:
+        return False, (_coords_code(coords),)
+    return True, (_coords_code(coords), _coords_code(coords2))
 
 
 def _require_cuda(t: torch.Tensor, name: str) -> None:
@@ -217,8 +235,9 @@ def _stream(dev: torch.device) -> int:
 
 
 def invariant_mass(v1: VecArg, v2: VecArg, out: Optional[torch.Tensor] = None,
-                   coords: str = "ptetaphim") -> torch.Tensor:
-    """InvariantMasses: ``out[i] = (v1[i] + v2[i]).mass()``, signed (ROOT convention)."""
+                   coords: str = "ptetaphim", coords2: Optional[str] = None) -> torch.Tensor:
+    """InvariantMasses: ``out[i] = (v1[i] + v2[i]).mass()``, signed (ROOT convention).
+    ``v1`` is in ``coords``; ``v2`` in ``coords2`` if given (mixed pairs), else in ``coords``."""
     a, n, dt, dev, k1 = _view(v1, 4, "v1")
     b, n2, dt2, dev2, k2 = _view(v2, 4, "v2")
     if n != n2:
@@ -232,8 +251,10 @@ def invariant_mass(v1: VecArg, v2: VecArg, out: Optional[torch.Tensor] = None,
         if out.shape != (n,) or out.dtype != dt or not out.is_contiguous() or out.device != dev:
             raise ValueError("out must be a contiguous [N] tensor of the inputs' dtype and device")
     with torch.cuda.device(dev):
-        _check(lib.gvx_invariant_mass(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b),
-                                      out.data_ptr() if n else None, n, _stream(dev)), "gvx_invariant_mass")
+        mixed, cc = _coords_args(coords, coords2)
+        fn = lib.gvx_invariant_mass_mixed if mixed else lib.gvx_invariant_mass
+        _check(fn(_dtype_code(dt), *cc, ctypes.byref(a), ctypes.byref(b), out.data_ptr() if n else None, n,
+                  _stream(dev)), "gvx_invariant_mass")
     return out
 
 
@@ -296,7 +317,7 @@ def new_bins(nbins: int = DEFAULT_NBINS, device=None) -> torch.Tensor:
 def mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = DEFAULT_HI,
                    nbins: int = DEFAULT_NBINS, bins: Optional[torch.Tensor] = None, cm: bool = False,
                    m_out: Optional[torch.Tensor] = None, boosted_out: Optional[VecArg] = None,
-                   coords: str = "ptetaphim") -> torch.Tensor:
+                   coords: str = "ptetaphim", coords2: Optional[str] = None) -> torch.Tensor:
     """Fused mass histogram (north star). Accumulates into ``bins`` ([nbins+2] int64, zeroed by the caller
     or allocated here) and returns it. ``cm=True`` boosts each pair to its CM frame first.
     ``boosted_out`` ([2N, 4], CM only) receives the boosted pair (vectors 2i, 2i+1)."""
@@ -327,9 +348,10 @@ def mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = D
         bo_ref = ctypes.byref(bo)
     flags = GVX_HIST_BOOST_TO_CM if cm else 0
     with torch.cuda.device(dev):
-        _check(lib.gvx_mass_histogram(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b), n,
-                                      float(lo), float(hi), int(nbins), bins.data_ptr(), flags, mptr, bo_ref,
-                                      _stream(dev)), "gvx_mass_histogram")
+        mixed, cc = _coords_args(coords, coords2)
+        fn = lib.gvx_mass_histogram_mixed if mixed else lib.gvx_mass_histogram
+        _check(fn(_dtype_code(dt), *cc, ctypes.byref(a), ctypes.byref(b), n, float(lo), float(hi), int(nbins),
+                  bins.data_ptr(), flags, mptr, bo_ref, _stream(dev)), "gvx_mass_histogram")
     return bins
 
 
@@ -421,7 +443,8 @@ def sharded_mass_histogram(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: f
 def pair_histograms(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = DEFAULT_HI,
                     nbins: int = DEFAULT_NBINS, lab_bins: Optional[torch.Tensor] = None,
                     cm_bins: Optional[torch.Tensor] = None, m_out: Optional[torch.Tensor] = None,
-                    cm_m_out: Optional[torch.Tensor] = None, coords: str = "ptetaphim"):
+                    cm_m_out: Optional[torch.Tensor] = None, coords: str = "ptetaphim",
+                    coords2: Optional[str] = None):
     """gvx_pair_histograms: lab mass + lab histogram + CM mass + CM histogram of the pairs in ONE
     pass over the inputs (bit-identical to invariant_mass / mass_histogram / mass_histogram(cm=True)).
     Returns ``(lab_bins, cm_bins)`` ([nbins+2] int64 each, accumulated)."""
@@ -436,9 +459,10 @@ def pair_histograms(v1: VecArg, v2: VecArg, lo: float = DEFAULT_LO, hi: float = 
     mptr = _out_1d(m_out, n, dt, "m_out")
     cptr = _out_1d(cm_m_out, n, dt, "cm_m_out")
     with torch.cuda.device(dev):
-        _check(lib.gvx_pair_histograms(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b), n,
-                                       float(lo), float(hi), int(nbins), lab_bins.data_ptr(), cm_bins.data_ptr(),
-                                       mptr, cptr, _stream(dev)), "gvx_pair_histograms")
+        mixed, cc = _coords_args(coords, coords2)
+        fn = lib.gvx_pair_histograms_mixed if mixed else lib.gvx_pair_histograms
+        _check(fn(_dtype_code(dt), *cc, ctypes.byref(a), ctypes.byref(b), n, float(lo), float(hi), int(nbins),
+                  lab_bins.data_ptr(), cm_bins.data_ptr(), mptr, cptr, _stream(dev)), "gvx_pair_histograms")
     return lab_bins, cm_bins
 
 
@@ -446,7 +470,7 @@ def pair_histograms_boost(v1: VecArg, v2: VecArg, bv: VecArg, beta: VecArg, lo: 
                           hi: float = DEFAULT_HI, nbins: int = DEFAULT_NBINS, lab_bins: Optional[torch.Tensor] = None,
                           cm_bins: Optional[torch.Tensor] = None, m_out: Optional[torch.Tensor] = None,
                           cm_m_out: Optional[torch.Tensor] = None, out: Optional[VecArg] = None,
-                          coords: str = "ptetaphim"):
+                          coords: str = "ptetaphim", coords2: Optional[str] = None):
     """gvx_pair_histograms_boost: pair_histograms(v1, v2) and boost(bv, beta) in ONE launch
     (bit-identical to the two calls). Returns ``(lab_bins, cm_bins, boosted)``."""
     a, n, dt, dev, _ = _view(v1, 4, "v1")
@@ -465,10 +489,11 @@ def pair_histograms_boost(v1: VecArg, v2: VecArg, bv: VecArg, beta: VecArg, lo: 
     cptr = _out_1d(cm_m_out, n, dt, "cm_m_out")
     out, o = _boost_out(bv, nb, dt, dev, out)
     with torch.cuda.device(dev):
-        _check(lib.gvx_pair_histograms_boost(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b),
-                                             n, float(lo), float(hi), int(nbins), lab_bins.data_ptr(),
-                                             cm_bins.data_ptr(), mptr, cptr, ctypes.byref(c), ctypes.byref(d),
-                                             ctypes.byref(o), nb, _stream(dev)), "gvx_pair_histograms_boost")
+        mixed, cc = _coords_args(coords, coords2)
+        fn = lib.gvx_pair_histograms_boost_mixed if mixed else lib.gvx_pair_histograms_boost
+        _check(fn(_dtype_code(dt), *cc, ctypes.byref(a), ctypes.byref(b), n, float(lo), float(hi), int(nbins),
+                  lab_bins.data_ptr(), cm_bins.data_ptr(), mptr, cptr, ctypes.byref(c), ctypes.byref(d),
+                  ctypes.byref(o), nb, _stream(dev)), "gvx_pair_histograms_boost")
     return lab_bins, cm_bins, out
 
 

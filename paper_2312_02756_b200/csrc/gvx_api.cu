@@ -707,6 +707,50 @@ gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64
   return e == cudaSuccess ? GVX_OK : cuda_fail(e);
 }
 
+// ------------------------------------------------ mixed-coordinate pairs --
+// v1 in c1, v2 in c2 (c1 != c2): k_mixed_pairs. AoS views with
+// 32-byte rows take the 256-bit loads, every other view the scalar ones.
+template <typename T, int L, int MODE>
+gvx_status launch_mixed_l(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int c1, int c2, int64_t n,
+                          const HistParams& hp, unsigned long long* bins, void* m_out, const HistParams& hc,
+                          unsigned long long* cbins, void* cm_out, const gvx_vec4_view* bo, cudaStream_t s) {
+  constexpr int G = Group<T, L>::G;
+  const size_t nbt = MODE == PM_MASS ? 0 : (size_t)hp.nbins + 2 + (MODE == PM_BOTH ? (size_t)hc.nbins + 2 : 0);
+  const bool smem = MODE != PM_MASS && nbt <= kMaxSmemBins;
+  auto k = smem ? k_mixed_pairs<T, L, MODE, true> : k_mixed_pairs<T, L, MODE, false>;
+  const size_t sm = smem ? nbt * sizeof(unsigned int) : 0;
+  const int grid = grid_for(k, kBlock, sm, (int64_t)kBlock * G, n);
+  // per-CTA uint32 shared-memory counters: one launch covers at most grid * 2^31 events
+  const int64_t chunk = smem ? ((int64_t)grid << 31) : n;
+  const View4o<T> bov = mk4o<T>(bo);
+  for (int64_t off = 0; off < n; off += chunk) {
+    const int64_t cn = n - off < chunk ? n - off : chunk;
+    View4<T> a = mk4<T>(v1), b = mk4<T>(v2);
+    View4o<T> bo2 = bov;
+    for (int c = 0; c < 4; ++c) {
+      a.c[c] += off * a.s;
+      b.c[c] += off * b.s;
+      if (bo) bo2.c[c] += 2 * off * bo2.s;
+    }
+    k<<<grid, kBlock, sm, s>>>(a, b, c1, c2, cn, hp, bins, m_out ? (T*)m_out + off : nullptr, hc, cbins,
+                               cm_out ? (T*)cm_out + off : nullptr, bo2);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+template <typename T, int MODE>
+gvx_status launch_mixed(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int c1, int c2, int64_t n,
+                        const HistParams& hp, unsigned long long* bins, void* m_out, const HistParams& hc,
+                        unsigned long long* cbins, void* cm_out, const gvx_vec4_view* bo, cudaStream_t s) {
+  const size_t es = sizeof(T);
+  constexpr int G = Group<T, L_AOS>::G;
+  const bool outs_ok = (!m_out || aligned(m_out, G * es)) && (!cm_out || aligned(cm_out, G * es));
+  if (classify(v1, es) == L_AOS && classify(v2, es) == L_AOS && outs_ok)
+    return launch_mixed_l<T, L_AOS, MODE>(v1, v2, c1, c2, n, hp, bins, m_out, hc, cbins, cm_out, bo, s);
+  return launch_mixed_l<T, L_GEN, MODE>(v1, v2, c1, c2, n, hp, bins, m_out, hc, cbins, cm_out, bo, s);
+}
+
 }  // namespace
 
 extern "C" {
@@ -978,6 +1022,110 @@ static gvx_status mass_histogram_impl(gvx_dtype dtype, gvx_coords coords, const 
   GVX_HIST_COORDS(float)
 #undef GVX_HIST_COORDS
 #undef GVX_HIST_DISPATCH
+}
+
+
+// ---------------------------------------------------------------------------
+// Mixed-coordinate entry points (ABI v7): v1 in coords1, v2 in coords2. Equal
+// systems take the single-system entry points above (same kernels, same bits).
+// ---------------------------------------------------------------------------
+gvx_status gvx_invariant_mass_mixed(gvx_dtype dtype, gvx_coords coords1, gvx_coords coords2,
+                                    const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, void* m_out, int64_t n,
+                                    gvx_stream_t stream) {
+  if (!valid_coords(coords1) || !valid_coords(coords2)) return GVX_ERR_INVALID_ARGUMENT;
+  if (coords1 == coords2) return gvx_invariant_mass(dtype, coords1, v1, v2, m_out, n, stream);
+  if (!valid_dtype(dtype) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GVX_OK;
+  const size_t es = dsize(dtype);
+  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !m_out || !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  const HistParams none = make_hist_params(0.0, 1.0, 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GVX_F64)
+    return launch_mixed<double, PM_MASS>(v1, v2, coords1, coords2, n, none, nullptr, m_out, none, nullptr, nullptr,
+                                         nullptr, s);
+  return launch_mixed<float, PM_MASS>(v1, v2, coords1, coords2, n, none, nullptr, m_out, none, nullptr, nullptr,
+                                      nullptr, s);
+}
+
+gvx_status gvx_mass_histogram_mixed(gvx_dtype dtype, gvx_coords coords1, gvx_coords coords2,
+                                    const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, double lo,
+                                    double hi, int32_t nbins, unsigned long long* bins, uint32_t flags, void* m_out,
+                                    const gvx_vec4_view* boosted_out, gvx_stream_t stream) {
+  if (!valid_coords(coords1) || !valid_coords(coords2)) return GVX_ERR_INVALID_ARGUMENT;
+  if (coords1 == coords2)
+    return gvx_mass_histogram(dtype, coords1, v1, v2, n, lo, hi, nbins, bins, flags, m_out, boosted_out, stream);
+  if (!valid_dtype(dtype) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
+  if ((flags & ~GVX_HIST_BOOST_TO_CM) != 0u) return GVX_ERR_INVALID_ARGUMENT;
+  const bool cm = (flags & GVX_HIST_BOOST_TO_CM) != 0u;
+  if (boosted_out && !cm) return GVX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GVX_OK;
+  const size_t es = dsize(dtype);
+  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !bins || !aligned(bins, 8)) return GVX_ERR_INVALID_ARGUMENT;
+  if (m_out && !aligned(m_out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  if (boosted_out && !out_view_ok(boosted_out, es)) return GVX_ERR_INVALID_ARGUMENT;
+  const HistParams hp = make_hist_params(lo, hi, nbins);
+  cudaStream_t s = (cudaStream_t)stream;
+#define GVX_MIXED_HIST(T)                                                                                        \
+  return cm ? launch_mixed<T, PM_HIST_CM>(v1, v2, coords1, coords2, n, hp, bins, m_out, hp, nullptr, nullptr,   \
+                                          boosted_out, s)                                                        \
+            : launch_mixed<T, PM_HIST>(v1, v2, coords1, coords2, n, hp, bins, m_out, hp, nullptr, nullptr, nullptr, s);
+  if (dtype == GVX_F64) {
+    GVX_MIXED_HIST(double)
+  }
+  GVX_MIXED_HIST(float)
+#undef GVX_MIXED_HIST
+}
+
+gvx_status gvx_pair_histograms_mixed(gvx_dtype dtype, gvx_coords coords1, gvx_coords coords2,
+                                     const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, double lo,
+                                     double hi, int32_t nbins, unsigned long long* lab_bins,
+                                     unsigned long long* cm_bins, void* m_out, void* cm_m_out, gvx_stream_t stream) {
+  if (!valid_coords(coords1) || !valid_coords(coords2)) return GVX_ERR_INVALID_ARGUMENT;
+  if (coords1 == coords2)
+    return gvx_pair_histograms(dtype, coords1, v1, v2, n, lo, hi, nbins, lab_bins, cm_bins, m_out, cm_m_out, stream);
+  if (!valid_dtype(dtype) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GVX_OK;
+  const size_t es = dsize(dtype);
+  if (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !lab_bins || !aligned(lab_bins, 8) || !cm_bins ||
+      !aligned(cm_bins, 8))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if ((m_out && !aligned(m_out, es)) || (cm_m_out && !aligned(cm_m_out, es))) return GVX_ERR_INVALID_ARGUMENT;
+  const HistParams hp = make_hist_params(lo, hi, nbins);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GVX_F64)
+    return launch_mixed<double, PM_BOTH>(v1, v2, coords1, coords2, n, hp, lab_bins, m_out, hp, cm_bins, cm_m_out,
+                                         nullptr, s);
+  return launch_mixed<float, PM_BOTH>(v1, v2, coords1, coords2, n, hp, lab_bins, m_out, hp, cm_bins, cm_m_out,
+                                      nullptr, s);
+}
+
+gvx_status gvx_pair_histograms_boost_mixed(gvx_dtype dtype, gvx_coords coords1, gvx_coords coords2,
+                                           const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64_t n, double lo,
+                                           double hi, int32_t nbins, unsigned long long* lab_bins,
+                                           unsigned long long* cm_bins, void* m_out, void* cm_m_out,
+                                           const gvx_vec4_cview* bv, const gvx_vec3_cview* beta,
+                                           const gvx_vec4_view* bout, int64_t nb, gvx_stream_t stream) {
+  if (!valid_coords(coords1) || !valid_coords(coords2)) return GVX_ERR_INVALID_ARGUMENT;
+  if (coords1 == coords2)
+    return gvx_pair_histograms_boost(dtype, coords1, v1, v2, n, lo, hi, nbins, lab_bins, cm_bins, m_out, cm_m_out,
+                                     bv, beta, bout, nb, stream);
+  // validate both halves before enqueueing either
+  if (!valid_dtype(dtype) || n < 0 || nb < 0) return GVX_ERR_INVALID_ARGUMENT;
+  if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
+  const size_t es = dsize(dtype);
+  if (nb > 0 && (!view_ok<4>(bv, es) || !view_ok<3>(beta, es) || !out_view_ok(bout, es)))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if (n > 0 && (!view_ok<4>(v1, es) || !view_ok<4>(v2, es) || !lab_bins || !aligned(lab_bins, 8) || !cm_bins ||
+                !aligned(cm_bins, 8)))
+    return GVX_ERR_INVALID_ARGUMENT;
+  if ((m_out && !aligned(m_out, es)) || (cm_m_out && !aligned(cm_m_out, es))) return GVX_ERR_INVALID_ARGUMENT;
+  gvx_status st = n > 0 ? gvx_pair_histograms_mixed(dtype, coords1, coords2, v1, v2, n, lo, hi, nbins, lab_bins,
+                                                    cm_bins, m_out, cm_m_out, stream)
+                        : GVX_OK;
+  if (st != GVX_OK || nb == 0) return st;
+  return gvx_boost(dtype, bv, beta, bout, nb, stream);
 }
 
 }  // extern "C"

@@ -20,6 +20,10 @@ namespace gvx {
 
 enum Layout { L_AOS = 0, L_SOA = 1, L_GEN = 2 };
 enum Coords { C_PTETAPHIM = 0, C_PXPYPZE = 1, C_PXPYPZM = 2, C_PTETAPHIE = 3 };
+// What a pair kernel produces. PM_BOTH: lab mass + lab histogram + CM mass + CM
+// histogram in one pass over the pairs (gvx_pair_histograms); in k_pair_tma the
+// CM histogram and masses use the CosOut slot.
+enum PairMode { PM_MASS = 0, PM_HIST = 1, PM_HIST_CM = 2, PM_HIST_CM_COS = 3, PM_BOTH = 4 };
 
 template <typename T> struct View4 { const T* c[4]; int64_t s; };
 template <typename T> struct View4o { T* c[4]; int64_t s; };
@@ -405,6 +409,120 @@ __global__ void __launch_bounds__(256) k_cm_costheta(View4<T> v1, View4<T> v2, i
 }
 
 // ============================================================================
+// Mixed-coordinate pairs (the kernel takes "two
+// particles expressed in any 4-dimensional coordinate system"; SPEC.md:305:
+// the result does not depend on the systems of the operands). v1 is in system
+// c1 and v2 in c2 (kernel arguments: warp-uniform branches, so one instantiation
+// per mode covers the 12 mixed combinations). Each vector is converted to
+// PxPyPzE on its own with the same conversions the single-system kernels use
+// (fast domain + literal cold path), then summed and its signed mass taken
+// literally (mass_of_sum: E^2 - |P|^2); the CM modes boost
+// the pair with cm_pair_mass (reading R11). Same-system pairs never come here:
+// they keep the reduced-form kernels above (the ABI dispatches on c1 == c2).
+//   MODE  PM_MASS: m_out;  PM_HIST / PM_HIST_CM: lab / CM mass -> bins (+ m_out,
+//         + boosted pair for CM);  PM_BOTH: lab -> bins + m_out, CM -> co.bins +
+//         co.cos_out (the fused pair pass of gvx_pair_histograms).
+//   SMEM  histograms privatised in shared memory (else global atomics).
+// ============================================================================
+template <typename T>
+__device__ __forceinline__ V4<T> to_cartesian_rt(int c, const T (&a)[4]) {
+  if (c == C_PTETAPHIM) return ptetaphim_to_cartesian(a[0], a[1], a[2], a[3]);
+  if (c == C_PXPYPZM) return pxpypzm_to_cartesian(a[0], a[1], a[2], a[3]);
+  if (c == C_PTETAPHIE) return ptetaphie_to_cartesian(a[0], a[1], a[2], a[3]);
+  return V4<T>{a[0], a[1], a[2], a[3]};
+}
+
+template <typename T, int L, int MODE, bool SMEM>
+__global__ void __launch_bounds__(256) k_mixed_pairs(View4<T> v1, View4<T> v2, int c1, int c2, int64_t n,
+                                                     HistParams hp, unsigned long long* __restrict__ bins,
+                                                     T* __restrict__ m_out, HistParams hc,
+                                                     unsigned long long* __restrict__ cbins, T* __restrict__ cm_out,
+                                                     View4o<T> bo) {
+  extern __shared__ unsigned int shx[];
+  constexpr int G = Group<T, L>::G;
+  static_assert(MODE == PM_MASS || MODE == PM_HIST || MODE == PM_HIST_CM || MODE == PM_BOTH, "mode");
+  constexpr bool HIST = MODE != PM_MASS;
+  constexpr bool TWO = MODE == PM_BOTH;
+  constexpr bool CM = MODE == PM_HIST_CM || TWO;
+  const int nb2 = hp.nbins + 2;
+  const int nbt = HIST ? nb2 + (TWO ? hc.nbins + 2 : 0) : 0;
+  if constexpr (SMEM && HIST) {
+    for (int b = threadIdx.x; b < nbt; b += blockDim.x) shx[b] = 0u;
+    __syncthreads();
+  }
+  auto count = [&](T M, bool second) {
+    if constexpr (SMEM) {
+      atomicAdd(&shx[second ? nb2 + find_bin(M, hc) : find_bin(M, hp)], 1u);
+    } else {
+      if (second) atomicAdd(&cbins[find_bin(M, hc)], 1ull);
+      else hist_flush(bins, hp, find_bin(M, hp), 1ull);
+    }
+  };
+  auto event = [&](const T (&x)[4], const T (&y)[4], int64_t i) {
+    const V4<T> a = to_cartesian_rt(c1, x), b = to_cartesian_rt(c2, y);
+    T ml = T(0), mc = T(0);
+    if constexpr (MODE != PM_HIST_CM) ml = mass_of_sum(a, b);
+    if constexpr (CM) {
+      V4<T> a2, b2;
+      const bool wbo = !TWO && bo.c[0] != nullptr;
+      mc = cm_pair_mass<T>(a, b, wbo ? &a2 : nullptr, wbo ? &b2 : nullptr);
+      if (wbo) {
+        const int64_t j0 = (2 * i) * bo.s, j1 = (2 * i + 1) * bo.s;
+        bo.c[0][j0] = a2.x; bo.c[1][j0] = a2.y; bo.c[2][j0] = a2.z; bo.c[3][j0] = a2.t;
+        bo.c[0][j1] = b2.x; bo.c[1][j1] = b2.y; bo.c[2][j1] = b2.z; bo.c[3][j1] = b2.t;
+      }
+    }
+    if constexpr (MODE == PM_MASS) {
+      m_out[i] = ml;
+    } else if constexpr (MODE == PM_HIST) {
+      count(ml, false);
+      if (m_out) m_out[i] = ml;
+    } else if constexpr (MODE == PM_HIST_CM) {
+      count(mc, false);
+      if (m_out) m_out[i] = mc;
+    } else {
+      count(ml, false);
+      count(mc, true);
+      if (m_out) m_out[i] = ml;
+      if (cm_out) cm_out[i] = mc;
+    }
+  };
+  const int64_t ngroups = n / G;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t g = tid; g < ngroups; g += nthr) {
+    T a[4][G], b[4][G];
+    load_group<T, L>(v1, g, a);
+    load_group<T, L>(v2, g, b);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      T x[4] = {a[0][j], a[1][j], a[2][j], a[3][j]};
+      T y[4] = {b[0][j], b[1][j], b[2][j], b[3][j]};
+      event(x, y, g * G + j);
+    }
+  }
+  if constexpr (G > 1) {
+    const int64_t i = ngroups * G + tid;
+    if (i < n) {
+      T x[4], y[4];
+      load_event(v1, i, x);
+      load_event(v2, i, y);
+      event(x, y, i);
+    }
+  }
+  if constexpr (SMEM && HIST) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbt; b += blockDim.x) {
+      const unsigned int c = shx[b];
+      if (c) {
+        if (b < nb2) hist_flush(bins, hp, b, c);
+        else atomicAdd(&cbins[b - nb2], (unsigned long long)c);
+      }
+    }
+  }
+}
+
+// ============================================================================
 // Jagged dimuon selection + mass histogram (DESIGN R21):
 // event e owns muons [offsets[e], offsets[e+1]); selected iff exactly two
 // muons of opposite charge; the pair mass is binned (shared-memory bins).
@@ -760,9 +878,6 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
 // HBM reads for later stages stay in flight while the FP64 pipe works —
 // bytes in flight are set by STAGES x TILE, not by register occupancy.
 // ============================================================================
-// PM_BOTH: lab mass + lab histogram + CM mass + CM histogram in one pass over the
-// pairs (gvx_pair_histograms); the CM histogram and masses use the CosOut slot.
-enum PairMode { PM_MASS = 0, PM_HIST = 1, PM_HIST_CM = 2, PM_HIST_CM_COS = 3, PM_BOTH = 4 };
 
 template <typename T, int TILE_, int STAGES_, int NCW_, int MINB_ = 1>
 struct PairTma {

@@ -243,3 +243,56 @@ def test_binding_rejects_unsupported_strides(gvx, monkeypatch):
     monkeypatch.setattr(gvx, "_require_cuda", lambda x, name: None)
     with pytest.raises(ValueError, match="stride"):
         gvx._view(t, 4, "v1")
+
+
+def test_mixed_coords_validation(gvx):
+    """The mixed-coordinate entry points (ABI v7) validate both systems and the rest of their
+    arguments synchronously, exactly as the single-system calls; n == 0 launches nothing."""
+    L = gvx.lib
+    by = ctypes.byref
+    a, b = _view(), _view()
+    PM, PE = gvx.GVX_PTETAPHIM, gvx.GVX_PXPYPZE
+    M = L.gvx_invariant_mass_mixed
+    assert M(gvx.GVX_F64, PM, 9, by(a), by(b), 0x2000, 4, None) == 1      # bad coords2
+    assert M(gvx.GVX_F64, 9, PE, by(a), by(b), 0x2000, 4, None) == 1      # bad coords1
+    assert M(gvx.GVX_F64, PM, PE, by(a), by(b), 0x2000, -1, None) == 1
+    assert M(7, PM, PE, by(a), by(b), 0x2000, 4, None) == 1
+    assert M(gvx.GVX_F64, PM, PE, by(a), by(b), None, 4, None) == 1       # NULL output
+    assert M(gvx.GVX_F64, PM, PE, by(_view(0x1004)), by(b), 0x2000, 4, None) == 1
+    assert M(gvx.GVX_F64, PM, PE, None, None, None, 0, None) == 0         # empty: OK
+    H = L.gvx_mass_histogram_mixed
+    assert H(gvx.GVX_F64, PM, PE, by(a), by(b), 4, 1.0, 1.0, 10, 0x4000, 0, None, None, None) == 1
+    assert H(gvx.GVX_F64, PM, PE, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 0x80, None, None, None) == 1
+    assert H(gvx.GVX_F64, PM, PE, by(a), by(b), 4, 0.0, 1.0, 10, None, 0, None, None, None) == 1
+    assert H(gvx.GVX_F64, PM, 5, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 0, None, None, None) == 1
+    assert H(gvx.GVX_F64, PM, PE, by(a), by(b), 0, 0.0, 1.0, 10, None, 0, None, None, None) == 0
+    P = L.gvx_pair_histograms_mixed
+    assert P(gvx.GVX_F32, PM, PE, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, None, None, None, None) == 1
+    assert P(gvx.GVX_F32, PM, PE, by(a), by(b), 4, 0.0, 1.0, 0, 0x4000, 0x5000, None, None, None) == 1
+    assert P(gvx.GVX_F32, PM, PE, by(a), by(b), 0, 0.0, 1.0, 10, None, None, None, None, None) == 0
+    beta = gvx.Vec3CView()
+    beta.c[0], beta.c[1], beta.c[2], beta.stride = 0x9000, 0x9008, 0x9010, 3
+    out = gvx.Vec4View()
+    for k in range(4):
+        out.c[k] = 0xA000 + 8 * k
+    out.stride = 4
+    F = L.gvx_pair_histograms_boost_mixed
+    assert F(gvx.GVX_F64, PM, PE, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 0x5000, None, None, by(a), by(beta),
+             by(out), -1, None) == 1
+    bad = gvx.Vec4View()
+    bad.c[0], bad.stride = 0xA001, 4
+    # a bad boost half is caught before the pair half is enqueued
+    assert F(gvx.GVX_F64, PM, PE, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 0x5000, None, None, by(a), by(beta),
+             by(bad), 4, None) == 1
+    assert F(gvx.GVX_F64, PM, PE, by(a), by(b), 0, 0.0, 1.0, 10, None, None, None, None, None, None, None, 0,
+             None) == 0
+
+
+def test_host_pipeline_validation(gvx):
+    """gvx_host_pairs validates coords and the axis before anything is enqueued (no pipeline
+    needed to reach these checks: a NULL pipeline is itself INVALID_ARGUMENT)."""
+    import paper_2312_02756_b200.hostpipe  # noqa: F401  (sets the host-pipeline argtypes)
+    L = gvx.lib
+    assert L.gvx_host_pairs(None, 0, 0x1000, 0x2000, 4, 0.0, 1.0, 10, None, 0x3000, None, None) == 1
+    assert L.gvx_host_pipeline_create(7, 1024, ctypes.byref(ctypes.c_void_p())) == 1
+    assert L.gvx_host_pipeline_create(gvx.GVX_F64, 0, ctypes.byref(ctypes.c_void_p())) == 1

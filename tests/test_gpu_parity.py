@@ -1208,3 +1208,93 @@ def test_one_launch_step_repeat_bitwise(gvx):
         assert torch.equal(lab, lab_ref) and torch.equal(cmb, cm_ref)
         assert torch.equal(m.view(torch.int64), m_ref.view(torch.int64))
         assert torch.equal(out.view(torch.int64), out_ref.view(torch.int64))
+
+
+# ----------------------------------------------------------------------------
+# Mixed-coordinate pairs (ABI v7; "any 4-dimensional coordinate system")
+# ----------------------------------------------------------------------------
+SYSTEMS = ("ptetaphim", "pxpypze", "pxpypzm", "ptetaphie")
+
+
+def as_system(v, system):
+    """Rewrite PtEtaPhiM vectors (f64) in `system` (numpy f64; input preparation, not the method)."""
+    pt, eta, phi, m = v[:, 0], v[:, 1], v[:, 2], v[:, 3]
+    px, py, pz = pt * np.cos(phi), pt * np.sin(phi), pt * np.sinh(eta)
+    E = np.sqrt(m * m + (pt * np.cosh(eta)) ** 2)
+    return {"ptetaphim": v, "pxpypze": np.stack([px, py, pz, E], 1), "pxpypzm": np.stack([px, py, pz, m], 1),
+            "ptetaphie": np.stack([pt, eta, phi, E], 1)}[system]
+
+
+def scale_of(O, v, system):
+    """max(E, |p|) of each vector in its own system (reading R5)."""
+    _, e = O.invariant_mass(v, np.zeros_like(v), coords=system)
+    a = v.astype(np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        p = np.abs(a[:, 0]) * np.cosh(a[:, 1]) if system.startswith("pt") else np.sqrt((a[:, :3] ** 2).sum(1))
+    return np.fmax(e.astype(np.float64), p)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_mixed_coordinate_pairs(gvx, O, dt):
+    """All 16 (system of v1, system of v2) combinations against the oracle: lab masses (AoS, SoA,
+    strided views), lab and CM histograms (R14), the fused pair pass and the one-call step; equal
+    systems through the mixed entry points are bit-identical to the single-system calls."""
+    n = 40_003
+    base1, base2 = synth.muon_pairs(np.arange(n), seed=404)
+    ea, eb = edge_events(np.float64)
+    tau = tau_of(dt)
+    for s1 in SYSTEMS:
+        for s2 in SYSTEMS:
+            with np.errstate(invalid="ignore", over="ignore"):
+                v1 = np.concatenate([as_system(ea, s1), as_system(base1, s1)]).astype(dt)
+                v2 = np.concatenate([as_system(eb, s2), as_system(base2, s2)]).astype(dt)
+            mo, _ = O.invariant_mass(v1, v2, coords=s1, coords2=s2)
+            e = scale_of(O, v1, s1) + scale_of(O, v2, s2)
+            t1, t2 = dev(v1), dev(v2)
+            m = host(gvx.invariant_mass(t1, t2, coords=s1, coords2=s2))
+            bad = mass_violations(m, mo, e, tau)
+            assert bad.size == 0, (s1, s2, bad[:5], m[bad[:5]], mo[bad[:5]])
+            soa = lambda t: [t[:, k].contiguous() for k in range(4)]  # noqa: E731
+            assert np.array_equal(host(gvx.invariant_mass(soa(t1), soa(t2), coords=s1, coords2=s2)), m, equal_nan=True)
+            pairs = torch.stack([t1, t2], dim=1).contiguous()
+            assert np.array_equal(host(gvx.invariant_mass(pairs[:, 0, :], pairs[:, 1, :], coords=s1, coords2=s2)), m,
+                                  equal_nan=True)
+            if s1 == s2:
+                assert np.array_equal(m, host(gvx.invariant_mass(t1, t2, coords=s1)), equal_nan=True)
+            for cm in (False, True):
+                mg = torch.empty(v1.shape[0], dtype=TDT[dt], device="cuda")
+                h = host(gvx.mass_histogram(t1, t2, cm=cm, coords=s1, coords2=s2, m_out=mg))
+                ho, mho = O.mass_histogram(v1, v2, LO, HI, NB, cm=cm, coords=s1, coords2=s2)
+                nanp = (np.isnan(mho) | (np.abs(mo.astype(np.float64)) < (1e-2 if dt == np.float32 else 1e-6) * e)) \
+                    if cm else None
+                fails, _ = hist_check(h, mho, e, tau, LO, HI, NB, nan_possible=nanp, m_window_center=mo if cm else None)
+                assert not fails, (s1, s2, cm, fails)
+                ok = ~nanp if cm else np.ones(v1.shape[0], bool)
+                assert mass_violations(host(mg)[ok], mho[ok], e[ok], tau).size == 0, (s1, s2, cm)
+                assert np.array_equal(h, np.bincount(find_bin_np(host(mg), LO, HI, NB), minlength=NB + 2))
+            # the fused pair pass and the one-call step: the same bins and masses as the calls above
+            ml, mc = (torch.empty(v1.shape[0], dtype=TDT[dt], device="cuda") for _ in range(2))
+            lab, cmb = gvx.pair_histograms(t1, t2, coords=s1, coords2=s2, m_out=ml, cm_m_out=mc)
+            assert np.array_equal(host(ml), m, equal_nan=True)
+            mcs = torch.empty_like(mc)
+            assert torch.equal(gvx.mass_histogram(t1, t2, coords=s1, coords2=s2), lab)
+            assert torch.equal(gvx.mass_histogram(t1, t2, cm=True, coords=s1, coords2=s2, m_out=mcs), cmb)
+            assert np.array_equal(host(mc), host(mcs), equal_nan=True)
+            bv, bb = synth.boost_inputs(np.arange(1000), dtype=dt)
+            lab2, cmb2, out = gvx.pair_histograms_boost(t1, t2, dev(bv), dev(bb), coords=s1, coords2=s2)
+            assert torch.equal(lab2, lab) and torch.equal(cmb2, cmb)
+            assert np.array_equal(host(out), host(gvx.boost(dev(bv), dev(bb))), equal_nan=True)
+
+
+def test_mixed_coordinate_pair_closed_form(gvx):
+    """SPEC.md:88's vector (PtEtaPhiM) against its mirror image in PxPyPzE as S:88 prints it:
+    back to back with equal energies, M = 2E (f64 to τ·E²)."""
+    a = torch.tensor([[10.0, 1.2, 0.5, 0.105]] * 5, dtype=torch.float64, device="cuda")
+    b = torch.tensor([[-8.7758256189037271612, -4.7942553860420300027, -15.09461355412172616,
+                       18.106860118426809386]] * 5, dtype=torch.float64, device="cuda")
+    m = host(gvx.invariant_mass(a, b, coords="ptetaphim", coords2="pxpypze"))
+    E = 2 * 18.106860118426809386
+    assert np.all(np.abs(m * m - E * E) <= 1e-12 * E * E), m
+    mc = torch.empty(5, dtype=torch.float64, device="cuda")
+    gvx.mass_histogram(a, b, cm=True, coords="ptetaphim", coords2="pxpypze", m_out=mc)
+    assert np.all(np.abs(host(mc) ** 2 - E * E) <= 1e-12 * E * E)

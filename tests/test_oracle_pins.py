@@ -791,3 +791,88 @@ def test_cm_negative_energy_pair_has_no_rest_frame(O):
     # the lab mass of the same pair is defined: E² − p² = 64 → 8
     ml, _ = O.invariant_mass(a, b, coords="pxpypze")
     assert ml[0] == 8.0
+
+
+# --------------------------------------------------------------------------
+# Mixed-coordinate pairs ("two particles expressed in any 4-dimensional
+# coordinate system")
+# --------------------------------------------------------------------------
+
+SYSTEMS = ("ptetaphim", "pxpypze", "pxpypzm", "ptetaphie")
+
+
+def mp_cartesian(system, comps):
+    """40-digit PxPyPzE of a vector given in `system` (R2 clamp)."""
+    a, b, c, d = (mp.mpf(float(x)) for x in comps)
+    if system in ("ptetaphim", "ptetaphie"):
+        px, py, pz = a * mp.cos(c), a * mp.sin(c), a * mp.sinh(b)
+        if system == "ptetaphie":
+            return px, py, pz, d
+        e2 = d * abs(d) + a * a + pz * pz
+        return px, py, pz, mp.sqrt(max(e2, 0))
+    if system == "pxpypze":
+        return a, b, c, d
+    e2 = a * a + b * b + c * c + d * abs(d)
+    return a, b, c, mp.sqrt(max(e2, 0))
+
+
+def represent(system, pt, eta, phi, m):
+    """The physics vector (pt, η, φ, m) written in `system` at 40 digits, then rounded."""
+    pt, eta, phi, m = (mp.mpf(float(x)) for x in (pt, eta, phi, m))
+    px, py, pz = pt * mp.cos(phi), pt * mp.sin(phi), pt * mp.sinh(eta)
+    E = mp.sqrt(m * m + (pt * mp.cosh(eta)) ** 2)
+    return {"ptetaphim": (pt, eta, phi, m), "pxpypze": (px, py, pz, E), "pxpypzm": (px, py, pz, m),
+            "ptetaphie": (pt, eta, phi, E)}[system]
+
+
+def test_mixed_pair_closed_form(O):
+    """SPEC.md:88's vector in PtEtaPhiM and its mirror image in PxPyPzE with the components S:88
+    prints, (−px, −py, −pz, E): back to back with equal energies, so M = 2E (to the 20 printed
+    digits). A swapped or mis-signed Cartesian component anywhere breaks it by O(1)."""
+    a = np.array([[10.0, 1.2, 0.5, 0.105]])
+    b = np.array([[-8.7758256189037271612, -4.7942553860420300027, -15.09461355412172616, 18.106860118426809386]])
+    for dt in (np.float64, np.float32):
+        m, e = O.invariant_mass(a.astype(dt), b.astype(dt), coords="ptetaphim", coords2="pxpypze")
+        assert e[0] == pytest.approx(2 * 18.106860118426809386, rel=4 * np.finfo(dt).eps)
+        tau = 1e-12 if dt == np.float64 else 1e-5
+        assert abs(float(m[0]) ** 2 - (2 * 18.106860118426809386) ** 2) <= tau * float(e[0]) ** 2, (dt, m[0])
+        # the other order, and the CM path (already at rest: M_cm = M)
+        m2, _ = O.invariant_mass(b.astype(dt), a.astype(dt), coords="pxpypze", coords2="ptetaphim")
+        assert m2[0] == m[0]
+        mc, _ = O.cm_mass(a.astype(dt), b.astype(dt), coords="ptetaphim", coords2="pxpypze")
+        assert abs(float(mc[0]) ** 2 - (2 * 18.106860118426809386) ** 2) <= tau * float(e[0]) ** 2
+
+
+@pytest.mark.parametrize("dt,bound", [(np.float64, 1e-14), (np.float32, 2e-6)])
+def test_mixed_pairs_vs_cartesian_mpmath(O, dt, bound):
+    """Every (system of v1, system of v2) combination against the 40-digit all-Cartesian mass of the
+    same rounded inputs: |M²_oracle − M²_truth| ≤ bound·E_lab². The same physics pair written in
+    different systems gives the same mass to that bound. Lab and CM masses and the
+    histogram agree with the same-system calls when the systems coincide."""
+    v1, v2 = synth.muon_pairs(np.arange(60), seed=31)
+    for s1 in SYSTEMS:
+        for s2 in SYSTEMS:
+            a = np.array([[float(x) for x in represent(s1, *r)] for r in v1], dt)
+            b = np.array([[float(x) for x in represent(s2, *r)] for r in v2], dt)
+            m, e = O.invariant_mass(a, b, coords=s1, coords2=s2)
+            for i in range(len(m)):
+                p = mp_cartesian(s1, a[i])
+                q = mp_cartesian(s2, b[i])
+                E = p[3] + q[3]
+                M2 = E * E - sum((p[k] + q[k]) ** 2 for k in range(3))
+                err = abs(signed_sq(mp.mpf(float(m[i]))) - M2) / E ** 2
+                assert err <= bound, (s1, s2, i, float(err))
+                assert abs(mp.mpf(float(e[i])) - E) <= 8 * np.finfo(dt).eps * E
+            if s1 == s2:
+                ms, es = O.invariant_mass(a, b, coords=s1)
+                assert np.array_equal(ms, m) and np.array_equal(es, e)
+            # CM mass = lab mass (Lorentz invariance) for the mixed pair too
+            mc, _ = O.cm_mass(a, b, coords=s1, coords2=s2)
+            ok = np.isfinite(mc)
+            if dt == np.float64:
+                assert ok.all()
+            tau = 1e-12 if dt == np.float64 else 1e-5
+            assert np.all(np.abs(signed_sq(mc[ok].astype(np.float64)) - signed_sq(m[ok].astype(np.float64)))
+                          <= tau * e[ok].astype(np.float64) ** 2)
+            h, hm = O.mass_histogram(a, b, 0.25, 300.0, 1000, coords=s1, coords2=s2)
+            assert np.array_equal(hm, m) and int(h.sum()) == len(m)
