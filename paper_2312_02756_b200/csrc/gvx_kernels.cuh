@@ -432,6 +432,18 @@ __device__ __forceinline__ V4<T> to_cartesian_rt(int c, const T (&a)[4]) {
   return V4<T>{a[0], a[1], a[2], a[3]};
 }
 
+// The pair arithmetic of the mixed kernels out of line: every mode calls the same code, so
+// the fused pass (PM_BOTH) gives the bits of the separate mass / CM calls whatever the
+// compiler would contract or share across an inlined context.
+template <typename T>
+__device__ __noinline__ T mixed_lab_mass(V4<T> a, V4<T> b) {
+  return mass_of_sum(a, b);
+}
+template <typename T>
+__device__ __noinline__ T mixed_cm_mass(V4<T> a, V4<T> b, V4<T>* a2, V4<T>* b2) {
+  return cm_pair_mass<T>(a, b, a2, b2);
+}
+
 template <typename T, int L, int MODE, bool SMEM>
 __global__ void __launch_bounds__(256) k_mixed_pairs(View4<T> v1, View4<T> v2, int c1, int c2, int64_t n,
                                                      HistParams hp, unsigned long long* __restrict__ bins,
@@ -461,11 +473,11 @@ __global__ void __launch_bounds__(256) k_mixed_pairs(View4<T> v1, View4<T> v2, i
   auto event = [&](const T (&x)[4], const T (&y)[4], int64_t i) {
     const V4<T> a = to_cartesian_rt(c1, x), b = to_cartesian_rt(c2, y);
     T ml = T(0), mc = T(0);
-    if constexpr (MODE != PM_HIST_CM) ml = mass_of_sum(a, b);
+    if constexpr (MODE != PM_HIST_CM) ml = mixed_lab_mass(a, b);
     if constexpr (CM) {
       V4<T> a2, b2;
       const bool wbo = !TWO && bo.c[0] != nullptr;
-      mc = cm_pair_mass<T>(a, b, wbo ? &a2 : nullptr, wbo ? &b2 : nullptr);
+      mc = mixed_cm_mass(a, b, wbo ? &a2 : nullptr, wbo ? &b2 : nullptr);
       if (wbo) {
         const int64_t j0 = (2 * i) * bo.s, j1 = (2 * i + 1) * bo.s;
         bo.c[0][j0] = a2.x; bo.c[1][j0] = a2.y; bo.c[2][j0] = a2.z; bo.c[3][j0] = a2.t;

@@ -1279,11 +1279,11 @@ def test_mixed_coordinate_pairs(gvx, O, dt):
             mcs = torch.empty_like(mc)
             assert torch.equal(gvx.mass_histogram(t1, t2, coords=s1, coords2=s2), lab)
             assert torch.equal(gvx.mass_histogram(t1, t2, cm=True, coords=s1, coords2=s2, m_out=mcs), cmb)
-            assert np.array_equal(host(mc), host(mcs), equal_nan=True)
+            assert np.array_equal(host(mc), host(mcs), equal_nan=True), (s1, s2)
             bv, bb = synth.boost_inputs(np.arange(1000), dtype=dt)
             lab2, cmb2, out = gvx.pair_histograms_boost(t1, t2, dev(bv), dev(bb), coords=s1, coords2=s2)
-            assert torch.equal(lab2, lab) and torch.equal(cmb2, cmb)
-            assert np.array_equal(host(out), host(gvx.boost(dev(bv), dev(bb))), equal_nan=True)
+            assert torch.equal(lab2, lab) and torch.equal(cmb2, cmb), (s1, s2)
+            assert np.array_equal(host(out), host(gvx.boost(dev(bv), dev(bb))), equal_nan=True), (s1, s2)
 
 
 def test_mixed_coordinate_pair_closed_form(gvx):
