@@ -65,6 +65,7 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-per-op", action="store_true", help="skip the per-op (mass / boost, f64 and f32) timings")
     p.add_argument("--cpu-sample", type=int, default=1 << 22, help="events in the oracle's bounded sample")
     p.add_argument("--dist-backend", default="nccl", help="process-group backend for N>1 (nccl on B200s)")
     p.add_argument("--two-launch", action="store_true",
@@ -462,6 +463,11 @@ def run_ours(args):
     del scratch
     for k in order:
         kernels[k]["frac_of_read_peak"] = kernels[k]["achieved_GBs"] / read_peak
+    # the metric's own numbers (InvariantMass / Boost at N), both dtypes, timed in this run after the step
+    per_op = None if args.no_per_op else run_per_op(args, gvx, sd, v1, v2, bv, bb, m, bout, n, dev, stream, peak,
+                                                    read_peak)
+    if per_op:
+        kernels.update(per_op)
     extended = run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak) if args.extended else None
 
     # e2e: the same step from pinned HOST buffers through the public API, copies timed
@@ -493,6 +499,56 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_per_op(args, gvx, sd, v1, v2, bv, bb, m, bout, n, dev, stream, peak, read_peak):
+    """BASELINE's metric names InvariantMass and Boost at N = 1e8: time each entry point on its own
+    (and the fused pair pass, and the step call of the other dtype) at the bench's N for f64 AND
+    f32, inputs resident in HBM (>> L2), CUDA events around each launch on the launch stream, mean
+    of --steps launches after two warm-ups. Keys "<op>_<dtype>"."""
+    import torch
+    out = {}
+    for dtn in ("f64", "f32"):
+        tdt = torch.float64 if dtn == "f64" else torch.float32
+        es = 8 if dtn == "f64" else 4
+        if dtn == args.dtype:
+            a1, a2, av, ab, am, ao = v1, v2, bv, bb, m, bout
+        else:
+            a1, a2 = sd.muon_pairs(n, first=0, dtype=tdt, device=dev)
+            av, ab = sd.boost_inputs(n, first=0, dtype=tdt, device=dev)
+            am = torch.empty(n, dtype=tdt, device=dev)
+            ao = torch.empty((n, 4), dtype=tdt, device=dev)
+        hb = torch.zeros(2 * (NB + 2), dtype=torch.int64, device=dev)
+        cases = {
+            "mass": (lambda: gvx.invariant_mass(a1, a2, out=am), BYTES["invariant_mass"](es), 1),
+            "boost": (lambda: gvx.boost(av, ab, out=ao), BYTES["boost"](es), 1),
+            "pairs": (lambda: gvx.pair_histograms(a1, a2, LO, HI, NB, lab_bins=hb[:NB + 2], cm_bins=hb[NB + 2:],
+                                                  m_out=am), BYTES["pairs"](es), 1),
+        }
+        if dtn != args.dtype or args.unfused or getattr(args, "two_launch", False):
+            cases["step"] = (lambda: gvx.pair_histograms_boost(a1, a2, av, ab, LO, HI, NB, lab_bins=hb[:NB + 2],
+                                                               cm_bins=hb[NB + 2:], m_out=am, out=ao),
+                             BYTES["step"](es), 1 if dtn == "f64" else 2)
+        for op, (fn, bpe, launches) in cases.items():
+            for _ in range(2):
+                fn()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for e0, e1 in evs:
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ts = [e0.elapsed_time(e1) for e0, e1 in evs]
+            ms = sum(ts) / len(ts)
+            gbs = n * bpe / (ms * 1e-3) / 1e9
+            out[f"{op}_{dtn}"] = {"ms": ms, "ms_best": min(ts), "events_per_s": n / (ms * 1e-3), "bytes_per_event": bpe,
+                                  "achieved_GBs": gbs, "frac_of_peak": gbs / peak, "frac_of_read_peak": gbs / read_peak,
+                                  "launches": launches}
+        if dtn != args.dtype:
+            del a1, a2, av, ab, am, ao
+            torch.cuda.empty_cache()
+    return out
 
 
 def run_extended(args, gvx, v1, v2, bv, bb, m, bout, n, es, stream, peak):
@@ -646,7 +702,10 @@ def gpu_time(fn, reps, flush):
     fn()
     torch.cuda.synchronize()
     for a, b in ev:
-        flush.fill_(1)  # 512 MB write: evicts the 126 MB L2
+        # evict the 126 MB L2 by READING 512 MB: the previous launch's dirty lines are written back
+        # here, outside the timed region, and L2 is left holding clean lines (a write-flush would
+        # leave 126 MB of dirty lines for the timed kernel to write back)
+        flush.sum(dtype=torch.int32)
         a.record()
         fn()
         b.record()
@@ -715,7 +774,7 @@ def run_sweep(args):
                     rec = {"op": what, "dtype": dtn, "layout": layout, "n": n, "gpu_ms_best": best,
                            "gpu_ms_median": med, "events_per_s": n / (best * 1e-3),
                            "GBs": n * bpe / (best * 1e-3) / 1e9, "cpu_1thread_ms": cpu, "cpu_kind": cpu_kind,
-                           "speedup_vs_1thread": cpu / best, "l2": "flushed (512 MB write) before each rep"}
+                           "speedup_vs_1thread": cpu / best, "l2": "flushed (512 MB read) before each rep"}
                     f.write(json.dumps(rec) + "\n")
                     f.flush()
                     print(json.dumps(rec))

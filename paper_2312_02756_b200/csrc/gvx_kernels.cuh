@@ -425,16 +425,17 @@ __global__ void __launch_bounds__(256) k_cm_costheta(View4<T> v1, View4<T> v2, i
 //   SMEM  histograms privatised in shared memory (else global atomics).
 // ============================================================================
 template <typename T>
-__device__ __forceinline__ V4<T> to_cartesian_rt(int c, const T (&a)[4]) {
+__device__ __noinline__ V4<T> to_cartesian_rt(int c, T a0, T a1, T a2, T a3) {
+  const T a[4] = {a0, a1, a2, a3};
   if (c == C_PTETAPHIM) return ptetaphim_to_cartesian(a[0], a[1], a[2], a[3]);
   if (c == C_PXPYPZM) return pxpypzm_to_cartesian(a[0], a[1], a[2], a[3]);
   if (c == C_PTETAPHIE) return ptetaphie_to_cartesian(a[0], a[1], a[2], a[3]);
   return V4<T>{a[0], a[1], a[2], a[3]};
 }
 
-// The pair arithmetic of the mixed kernels out of line: every mode calls the same code, so
-// the fused pass (PM_BOTH) gives the bits of the separate mass / CM calls whatever the
-// compiler would contract or share across an inlined context.
+// The arithmetic of the mixed kernels (the conversion above and these two) is out of line:
+// every mode calls the same code, so the fused pass (PM_BOTH) gives the bits of the separate
+// mass / CM calls whatever the compiler would contract or share in an inlined context.
 template <typename T>
 __device__ __noinline__ T mixed_lab_mass(V4<T> a, V4<T> b) {
   return mass_of_sum(a, b);
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(256) k_mixed_pairs(View4<T> v1, View4<T> v2, i
     }
   };
   auto event = [&](const T (&x)[4], const T (&y)[4], int64_t i) {
-    const V4<T> a = to_cartesian_rt(c1, x), b = to_cartesian_rt(c2, y);
+    const V4<T> a = to_cartesian_rt(c1, x[0], x[1], x[2], x[3]), b = to_cartesian_rt(c2, y[0], y[1], y[2], y[3]);
     T ml = T(0), mc = T(0);
     if constexpr (MODE != PM_HIST_CM) ml = mixed_lab_mass(a, b);
     if constexpr (CM) {
