@@ -81,6 +81,8 @@ def parse():
                    help="also time the widened rows (other coordinate systems, SoA, uniform boost) at N")
     p.add_argument("--sweep-out", default=os.path.join(ROOT, "gpurun_out", "nsweep.jsonl"))
     p.add_argument("--sweep-reps", type=int, default=10)
+    p.add_argument("--sweep-ns", default=None, help="comma-separated N values for --sweep (default: 1e4..1e8)")
+    p.add_argument("--sweep-dtypes", default="f64,f32")
     return p.parse_args()
 
 
@@ -738,14 +740,17 @@ def run_sweep(args):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     cpu_ms_per_event = {}
     with open(out_path, "w") as f:
+        ns = [int(float(x)) for x in args.sweep_ns.split(",")] if args.sweep_ns else SWEEP_NS
         for dtn, tdt, npdt, es in (("f64", torch.float64, np.float64, 8), ("f32", torch.float32, np.float32, 4)):
+            if dtn not in args.sweep_dtypes.split(","):
+                continue
             # oracle 1-thread cost per event (mass and boost), from N = 1e6 (paper's baseline)
             idx = np.arange(1_000_000)
             h1, h2 = synth.muon_pairs(idx, dtype=npdt)
             hv, hb = synth.boost_inputs(idx, dtype=npdt)
             cpu_ms_per_event[dtn] = {"mass": cpu_time(lambda: oracle.invariant_mass(h1, h2)) / 1e6,
                                      "boost": cpu_time(lambda: oracle.boost(hv, hb)) / 1e6}
-            for n in SWEEP_NS:
+            for n in ns:
                 v1, v2 = sd.muon_pairs(n, dtype=tdt)
                 bv, bb = sd.boost_inputs(n, dtype=tdt)
                 m = torch.empty(n, dtype=tdt, device="cuda")
