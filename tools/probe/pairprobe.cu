@@ -1,0 +1,288 @@
+// Fused pair pass (PM_BOTH, f64 PtEtaPhiM AoS) structure probe: the product
+// k_pair_tma against (B) setmaxnreg warp specialisation (a 4-warp producer
+// warpgroup shrunk to PREG registers, consumer warpgroups grown to CREG) and
+// (C) producer-free per-warp self-fed TMA rings. Every variant calls the same
+// pair_consume_x2 arithmetic, so its histograms must equal the product's
+// bit for bit. Standalone timing tool, not product code.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include <cuda_runtime.h>
+#include "../../paper_2312_02756_b200/csrc/gvx_kernels.cuh"
+using namespace gvx;
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
+
+__device__ __forceinline__ uint64_t mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double u01(uint64_t h) { return ((h >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
+
+__global__ void gen(double* v, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h0 = mix(seed * 0x9e3779b97f4a7c15ull + 4 * i), h1 = mix(h0 + 1), h2 = mix(h0 + 2), h3 = mix(h0 + 3);
+    double g = sqrt(-2.0 * log(u01(h0))) * cos(6.283185307179586 * u01(h1));
+    double pt = fmin(fmax(30.0 * exp(0.5 * g), 2.0), 2000.0);
+    v[4 * i] = pt;
+    v[4 * i + 1] = -2.5 + 5.0 * u01(h2);
+    v[4 * i + 2] = -3.141592653589793 + 6.283185307179586 * u01(h3);
+    v[4 * i + 3] = 0.1056583755;
+  }
+}
+
+template <int R> __device__ __forceinline__ void reg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R)); }
+template <int R> __device__ __forceinline__ void reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R)); }
+
+// (B) warp-specialised: warpgroup 0 = producer (warp 0 lane 0 issues), warpgroups 1..NCWG consume.
+template <int NCWG, int CREG, int PREG, int TILE, int STAGES>
+__global__ void __launch_bounds__(128 * (NCWG + 1), 1)
+    k_ws(View4<double> v1, View4<double> v2, int64_t n, double* __restrict__ m_out, HistParams hp,
+         unsigned long long* __restrict__ bins, View4o<double>, CosOut<double> co) {
+  constexpr int NCW = 4 * NCWG, NCT = NCW * 32, EPT = TILE / NCT, HALF = TILE * 32, TV = TILE * 4;
+  constexpr int RING = STAGES * 2 * HALF;
+  static_assert(TILE % NCT == 0 && EPT % 2 == 0, "geometry");
+  // setmaxnreg moves registers inside the CTA's launch allocation: the budget must fit it
+  constexpr int RL = (65536 / (128 * (NCWG + 1))) / 8 * 8;
+  static_assert(CREG == 0 || PREG + NCWG * CREG <= RL * (NCWG + 1), "setmaxnreg budget");
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING);
+  uint64_t* empty = full + STAGES;
+  unsigned int* sh_hist = reinterpret_cast<unsigned int*>(empty + STAGES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb2 = hp.nbins + 2, nbt = nb2 + co.hc.nbins + 2;
+  unsigned int* sh_cos = sh_hist + nb2;
+  for (int b = threadIdx.x; b < nbt; b += blockDim.x) sh_hist[b] = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { tma::mbar_init(&full[s], 1); tma::mbar_init(&empty[s], NCW); }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t ntiles = n / TILE;
+  if (warp < 4) {
+    if constexpr (PREG > 0) reg_dec<PREG>();
+    if (warp == 0 && lane == 0) {
+      const uint64_t pol = tma::policy_evict_first();
+      int s = 0, it = 0;
+      uint32_t ph = 1;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (it >= STAGES) { tma::mbar_wait(&empty[s], ph); tma::fence_proxy_async_smem(); }
+        tma::mbar_arrive_expect_tx(&full[s], 2 * HALF);
+        double* dst = ring + (size_t)s * 2 * TV;
+        tma::bulk_g2s(dst, v1.c[0] + t * TV, HALF, &full[s], pol);
+        tma::bulk_g2s(dst + TV, v2.c[0] + t * TV, HALF, &full[s], pol);
+        ++it;
+        if (++s == STAGES) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else {
+    if constexpr (CREG > 0) reg_inc<CREG>();
+    const int ctid = threadIdx.x - 128;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      tma::mbar_wait(&full[s], ph);
+      const double* src = ring + (size_t)s * 2 * TV;
+      double a[EPT][4], b[EPT][4];
+#pragma unroll
+      for (int u = 0; u < EPT; ++u) {
+        const int e = u * NCT + ctid;
+        lds_vec(src, e, lane, a[u]);
+        lds_vec(src + TV, e, lane, b[u]);
+      }
+      tma::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[s]);
+#pragma unroll
+      for (int u = 0; u < EPT; u += 2)
+        pair_consume_x2<C_PTETAPHIM, PM_BOTH>(a[u], b[u], a[u + 1], b[u + 1], t * TILE + u * NCT + ctid,
+                                             t * TILE + (u + 1) * NCT + ctid, m_out, sh_hist, hp,
+                                             View4o<double>{}, sh_cos, co);
+      if (++s == STAGES) { s = 0; ph ^= 1u; }
+    }
+    if (blockIdx.x == gridDim.x - 1) {
+      for (int64_t i = ntiles * TILE + ctid; i < n; i += NCT) {
+        double a[4], b[4];
+        for (int c = 0; c < 4; ++c) { a[c] = v1.c[0][4 * i + c]; b[c] = v2.c[0][4 * i + c]; }
+        pair_consume<double, C_PTETAPHIM, PM_BOTH, false>(a, b, i, m_out, sh_hist, hp, View4o<double>{}, sh_cos, co);
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbt; b += blockDim.x) {
+    unsigned int c = sh_hist[b];
+    if (c) {
+      if (b < nb2) atomicAdd(&bins[b], (unsigned long long)c);
+      else atomicAdd(&co.bins[b - nb2], (unsigned long long)c);
+    }
+  }
+}
+
+// (C) no producer warp: warp w of CTA c owns chunks (c * NW + w) + k * gridDim.x * NW of CH = 32 * EPT
+// events and streams them into its own S-deep ring (lane 0 issues; the warp's own loads order the refill).
+template <int NW, int S, int EPT, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB)
+    k_self(View4<double> v1, View4<double> v2, int64_t n, double* __restrict__ m_out, HistParams hp,
+           unsigned long long* __restrict__ bins, View4o<double>, CosOut<double> co) {
+  constexpr int CH = 32 * EPT, HALF = CH * 32, CV = CH * 4, STAGE = 2 * HALF;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ring = reinterpret_cast<double*>(smem) + (size_t)warp * S * 2 * CV;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NW * S * STAGE) + warp * S;
+  unsigned int* sh_hist = reinterpret_cast<unsigned int*>(reinterpret_cast<uint64_t*>(smem + (size_t)NW * S * STAGE) + NW * S);
+  const int nb2 = hp.nbins + 2, nbt = nb2 + co.hc.nbins + 2;
+  unsigned int* sh_cos = sh_hist + nb2;
+  for (int b = threadIdx.x; b < nbt; b += blockDim.x) sh_hist[b] = 0u;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) tma::mbar_init(&full[s], 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t nch = n / CH, step = (int64_t)gridDim.x * NW;
+  const int64_t c0 = (int64_t)blockIdx.x * NW + warp;
+  const uint64_t pol = tma::policy_evict_first();
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      const int64_t c = c0 + s * step;
+      if (c < nch) {
+        tma::mbar_arrive_expect_tx(&full[s], STAGE);
+        tma::bulk_g2s(ring + s * 2 * CV, v1.c[0] + c * CV, HALF, &full[s], pol);
+        tma::bulk_g2s(ring + s * 2 * CV + CV, v2.c[0] + c * CV, HALF, &full[s], pol);
+      }
+    }
+  }
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t c = c0; c < nch; c += step) {
+    tma::mbar_wait(&full[s], ph);
+    const double* src = ring + s * 2 * CV;
+    double a[EPT][4], b[EPT][4];
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      lds_vec(src, u * 32 + lane, lane, a[u]);
+      lds_vec(src + CV, u * 32 + lane, lane, b[u]);
+    }
+    tma::fence_proxy_async_smem();
+    __syncwarp();
+    const int64_t cn = c + S * step;
+    if (lane == 0 && cn < nch) {
+      tma::mbar_arrive_expect_tx(&full[s], STAGE);
+      tma::bulk_g2s(ring + s * 2 * CV, v1.c[0] + cn * CV, HALF, &full[s], pol);
+      tma::bulk_g2s(ring + s * 2 * CV + CV, v2.c[0] + cn * CV, HALF, &full[s], pol);
+    }
+#pragma unroll
+    for (int u = 0; u < EPT; u += 2)
+      pair_consume_x2<C_PTETAPHIM, PM_BOTH>(a[u], b[u], a[u + 1], b[u + 1], c * CH + u * 32 + lane,
+                                           c * CH + (u + 1) * 32 + lane, m_out, sh_hist, hp, View4o<double>{},
+                                           sh_cos, co);
+    if (++s == S) { s = 0; ph ^= 1u; }
+  }
+  if (blockIdx.x == gridDim.x - 1) {
+    for (int64_t i = nch * CH + threadIdx.x; i < n; i += blockDim.x) {
+      double a[4], b[4];
+      for (int k = 0; k < 4; ++k) { a[k] = v1.c[0][4 * i + k]; b[k] = v2.c[0][4 * i + k]; }
+      pair_consume<double, C_PTETAPHIM, PM_BOTH, false>(a, b, i, m_out, sh_hist, hp, View4o<double>{}, sh_cos, co);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbt; b += blockDim.x) {
+    unsigned int cc = sh_hist[b];
+    if (cc) {
+      if (b < nb2) atomicAdd(&bins[b], (unsigned long long)cc);
+      else atomicAdd(&co.bins[b - nb2], (unsigned long long)cc);
+    }
+  }
+}
+
+struct Ctx {
+  double *v1, *v2, *m;
+  int64_t n;
+  HistParams hp;
+  CosOut<double> co;
+  unsigned long long* bins;  // 2 * 1002
+  int sms;
+  cudaEvent_t e0, e1;
+  std::vector<unsigned long long> ref;
+  std::vector<double> mref;
+};
+
+template <typename K>
+void run(Ctx& c, const char* name, K k, int block, size_t smem, int per_sm_req) {
+  if (smem > 227 * 1024) { printf("%-40s smem %zu too large\n", name, smem); return; }
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, block, smem));
+  if (per < 1) { printf("%-40s does not fit (smem %zu)\n", name, smem); return; }
+  per = std::min(per, per_sm_req);
+  const int grid = c.sms * per;
+  View4<double> a{{c.v1, c.v1 + 1, c.v1 + 2, c.v1 + 3}, 4}, b{{c.v2, c.v2 + 1, c.v2 + 2, c.v2 + 3}, 4};
+  std::vector<float> ts;
+  for (int r = 0; r < 13; ++r) {
+    CK(cudaMemset(c.bins, 0, 2 * 1002 * 8));
+    CK(cudaEventRecord(c.e0));
+    k<<<grid, block, smem>>>(a, b, c.n, c.m, c.hp, c.bins, View4o<double>{}, c.co);
+    CK(cudaEventRecord(c.e1));
+    CK(cudaEventSynchronize(c.e1));
+    CK(cudaGetLastError());
+    float ms;
+    CK(cudaEventElapsedTime(&ms, c.e0, c.e1));
+    if (r >= 3) ts.push_back(ms);
+  }
+  std::sort(ts.begin(), ts.end());
+  std::vector<unsigned long long> h(2 * 1002);
+  CK(cudaMemcpy(h.data(), c.bins, h.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<double> m(1 << 20);
+  CK(cudaMemcpy(m.data(), c.m + c.n - m.size(), m.size() * 8, cudaMemcpyDeviceToHost));
+  const char* ok = "";
+  if (c.ref.empty()) { c.ref = h; c.mref = m; ok = "ref"; }
+  else ok = (h == c.ref && m == c.mref) ? "bit-equal" : "DIFFERENT";
+  const double gbs = 72.0 * c.n / (ts[0] * 1e6);
+  printf("%-40s grid %4d x %4d  best %.4f ms  median %.4f ms  %.0f GB/s  %s\n", name, grid, block, ts[0],
+         ts[ts.size() / 2], gbs, ok);
+  fflush(stdout);
+}
+
+int main(int argc, char** argv) {
+  Ctx c;
+  c.n = argc > 1 ? atoll(argv[1]) : 100000000LL;
+  const bool only_product = argc > 2 && argv[2][0] == 'p';
+  CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, 0));
+  CK(cudaMalloc(&c.v1, c.n * 32));
+  CK(cudaMalloc(&c.v2, c.n * 32));
+  CK(cudaMalloc(&c.m, c.n * 8));
+  CK(cudaMalloc(&c.bins, 2 * 1002 * 8));
+  gen<<<4 * c.sms, 256>>>(c.v1, c.n, 1);
+  gen<<<4 * c.sms, 256>>>(c.v2, c.n, 2);
+  CK(cudaDeviceSynchronize());
+  c.hp = make_hist_params(0.25, 300.0, 1000);
+  c.co = CosOut<double>{make_hist_params(0.25, 300.0, 1000), c.bins + 1002, nullptr};
+  CK(cudaEventCreate(&c.e0));
+  CK(cudaEventCreate(&c.e1));
+  const size_t hist = 2 * 1002 * 4;
+  {
+    using CFG = PairTma<double, 1536, 2, 24, 1>;
+    run(c, "product k_pair_tma 1536x2x24", k_pair_tma<double, C_PTETAPHIM, PM_BOTH, CFG, false, false>, 32 * 25,
+        CFG::smem_bytes(2004), 1);
+  }
+  if (only_product) return 0;
+#define WS(NCWG, CREG, PREG, TILE, ST)                                                                      \
+  run(c, "ws " #NCWG "wg c" #CREG " p" #PREG " " #TILE "x" #ST,                                           \
+      k_ws<NCWG, CREG, PREG, TILE, ST>, 128 * (NCWG + 1), (size_t)ST * TILE * 64 + ST * 16 + hist, 1)
+  WS(4, 112, 24, 1024, 3);
+  WS(3, 152, 24, 768, 4);
+#define SELF(NW, S, EPT, MINB)                                                                          \
+  run(c, "self " #NW "w s" #S " ept" #EPT " minb" #MINB, k_self<NW, S, EPT, MINB>, 32 * NW,             \
+      (size_t)NW * S * 64 * 32 * EPT + NW * S * 8 + hist, MINB)
+  SELF(24, 2, 2, 1);
+  SELF(26, 2, 2, 1);
+  SELF(28, 2, 2, 1);
+  SELF(32, 1, 2, 1);
+  SELF(16, 3, 2, 1);
+  SELF(20, 2, 2, 1);
+  SELF(12, 2, 2, 2);
+  SELF(24, 1, 4, 1);
+  return 0;
+}
