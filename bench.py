@@ -361,6 +361,8 @@ def run_ours(args):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(order) + 1)]
     kern_ms = {k: [] for k in order}
 
+    symm_out = []  # p2p: this rank's symmetric-memory bins of the last step
+
     def step(record: bool):
         bins_all.zero_()
         if record:
@@ -389,10 +391,10 @@ def run_ours(args):
         if record:
             ev[2].record(stream)
         if p2p:  # reduction fused into the histogram kernels (barriers included in their time)
-            gvx.allreduce_mass_histogram(v1, v2, LO, HI, NB, slot=0)
+            symm_out[:] = [gvx.allreduce_mass_histogram(v1, v2, LO, HI, NB, slot=0)]
             if record:
                 ev[3].record(stream)
-            gvx.allreduce_mass_histogram(v1, v2, LO, HI, NB, cm=True, slot=1)
+            symm_out.append(gvx.allreduce_mass_histogram(v1, v2, LO, HI, NB, cm=True, slot=1))
             if record:
                 ev[4].record(stream)
             return
@@ -427,6 +429,8 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
     elapsed_ms = t_start.elapsed_time(t_end)
+    # the last timed step's reduced histograms (lab, CM), for the G = 1 self-check below
+    reduced = torch.cat(symm_out).clone() if p2p else bins_all.clone()
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -477,6 +481,12 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, gvx, v1, v2, bv, bb, dev, stream, world)
 
+    # N > 1: the reduced bins must equal the one-GPU histogram of the same global indices
+    # (sharding changes nothing, bit for bit); rank 0 recomputes it shard by shard.
+    self_check = None
+    if world > 1 and rank == 0:
+        self_check = global_histogram_check(gvx, sd, reduced, n, world, tdt, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_obj(args.cpu_sample, args.dtype)
@@ -497,10 +507,28 @@ def run_ours(args):
             "step_hbm": {"algorithmic_bytes_per_gpu": step_bytes, "achieved_GBs_per_gpu": step_gbs,
                          "frac_of_peak": step_gbs / peak, "peak": peak},
             **({"extended": extended} if extended else {}),
+            **({"self_check": self_check} if self_check else {}),
         }
         print(json.dumps(line), flush=True)
+    if self_check and not self_check["bins_equal"]:
+        raise SystemExit("self-check failed: the reduced histograms differ from the one-GPU histogram")
     if world > 1:
         dist.destroy_process_group()
+
+
+def global_histogram_check(gvx, sd, reduced, n, world, tdt, dev):
+    """Rank 0, N > 1: the lab + CM histograms of the global index range [0, n * world), computed on
+    this GPU alone shard by shard (the one-GPU result), compared bit for bit with the reduced bins."""
+    import torch
+    ref = torch.zeros(2 * (NB + 2), dtype=torch.int64, device=dev)
+    for r in range(world):
+        a, b = sd.muon_pairs(n, first=r * n, dtype=tdt, device=dev)
+        gvx.pair_histograms(a, b, LO, HI, NB, lab_bins=ref[:NB + 2], cm_bins=ref[NB + 2:])
+        del a, b
+    torch.cuda.synchronize(dev)
+    diff = int((ref - reduced).abs().sum())
+    return {"bins_equal": diff == 0, "abs_diff_sum": diff, "events": n * world,
+            "what": "reduced lab+CM bins of the last timed step == one-GPU histogram of all global indices"}
 
 
 def run_per_op(args, gvx, sd, v1, v2, bv, bb, m, bout, n, dev, stream, peak, read_peak):

@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define GVX_ABI_VERSION 7
+#define GVX_ABI_VERSION 8
 
 typedef struct CUstream_st *gvx_stream_t; /* == cudaStream_t */
 
@@ -197,26 +197,34 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
 
 /*
  * gvx_mass_histogram_peers — gvx_mass_histogram with the cross-GPU bin
- * reduction fused into the kernel tail ("B200-native option"):
- * each CTA adds its final counts either
+ * reduction fused into the kernel tail ("B200-native option").
+ * Every CTA adds its privatised counts to `work`, a device-local workspace of
+ * nbins+3 uint64 (nbins+2 partial sums, then a ticket word); the CTA that
+ * finishes last reads-and-clears the partial sums and pushes each non-zero
+ * total once
  *   - to EVERY array of peer_bins[0 .. npeers-1] (a DEVICE array of device
  *     pointers, e.g. torch symmetric memory's buffer_ptrs_dev: P2P system-scope
  *     atomics over NVLink), or
- *   - once to mc_bins, an NVSwitch multicast address of the bins
- *     (multimem.red.add.u64; NVLS), when mc_bins != NULL (peer_bins ignored).
- * After every rank's call has completed (the caller's cross-rank barrier),
- * every rank's bins hold the global histogram: an all-reduce(SUM) without a
- * separate collective. Caller's contract: all ranks' bins are zeroed (or hold
- * the running totals) and visible before any rank launches (barrier), and no
- * rank reads them before the barrier that follows. Other arguments, binning
- * and errors as gvx_mass_histogram (boosted_out is not offered here);
- * peer_bins NULL / misaligned, npeers outside [1, 4096] -> INVALID_ARGUMENT.
+ *   - to mc_bins, an NVSwitch multicast address of the bins
+ *     (multimem.red.add.u64; NVLS), when mc_bins != NULL (peer_bins ignored),
+ * so a rank issues at most (nbins+2) x npeers remote adds (multicast: nbins+2)
+ * per launch, not one per CTA and bin. `work` must be all zero before the first
+ * call; every call leaves it all zero again (caller-owned, one per concurrently
+ * running call). After every rank's call has completed (the caller's cross-rank
+ * barrier), every rank's bins hold the global histogram: an all-reduce(SUM)
+ * without a separate collective. Caller's contract: all ranks' bins are zeroed
+ * (or hold the running totals) and visible before any rank launches (barrier),
+ * and no rank reads them before the barrier that follows. Other arguments,
+ * binning and errors as gvx_mass_histogram (boosted_out is not offered here);
+ * peer_bins NULL / misaligned, npeers outside [1, 4096], work NULL or
+ * misaligned -> INVALID_ARGUMENT.
  */
 gvx_status gvx_mass_histogram_peers(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview *v1,
                                     const gvx_vec4_cview *v2, int64_t n, double lo, double hi,
                                     int32_t nbins, unsigned long long *const *peer_bins,
-                                    int32_t npeers, unsigned long long *mc_bins, uint32_t flags,
-                                    void *m_out, gvx_stream_t stream);
+                                    int32_t npeers, unsigned long long *mc_bins,
+                                    unsigned long long *work, uint32_t flags, void *m_out,
+                                    gvx_stream_t stream);
 
 /*
  * gvx_cm_costheta_histogram — CM decay angle ("the CM path's

@@ -45,7 +45,7 @@ GVX_PXPYPZE = 1
 GVX_PXPYPZM = 2
 GVX_PTETAPHIE = 3
 GVX_HIST_BOOST_TO_CM = 0x1
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 # The default histogram of the north star: 1000 bins over the dimuon range
 # (reading R13).
@@ -112,7 +112,7 @@ def _load_lib():
     lib.gvx_pair_histograms_boost.restype = st
     lib.gvx_mass_histogram_peers.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
                                              ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, ctypes.c_int32,
-                                             P, ctypes.c_uint32, P, P]
+                                             P, P, ctypes.c_uint32, P, P]
     lib.gvx_mass_histogram_peers.restype = st
     lib.gvx_cm_costheta_histogram.argtypes = [st, st, ctypes.POINTER(Vec4CView), ctypes.POINTER(Vec4CView), I64,
                                               ctypes.c_double, ctypes.c_double, ctypes.c_int32, P,
@@ -497,14 +497,28 @@ def pair_histograms_boost(v1: VecArg, v2: VecArg, bv: VecArg, beta: VecArg, lo: 
     return lab_bins, cm_bins, out
 
 
+_PEER_WORK = {}
+
+
+def _peer_work(nbins: int, dev: torch.device, slot) -> torch.Tensor:
+    """The zeroed device workspace gvx_mass_histogram_peers pre-reduces into (nbins+2 partial
+    sums and a ticket word; every call leaves it zeroed), one per (device, nbins, slot)."""
+    key = (dev.index, nbins, slot)
+    if key not in _PEER_WORK:
+        _PEER_WORK[key] = torch.zeros(nbins + 3, dtype=torch.int64, device=dev)
+    return _PEER_WORK[key]
+
+
 def mass_histogram_peers(v1: VecArg, v2: VecArg, peer_bins_dev: int, npeers: int, lo: float = DEFAULT_LO,
                          hi: float = DEFAULT_HI, nbins: int = DEFAULT_NBINS, cm: bool = False,
                          m_out: Optional[torch.Tensor] = None, coords: str = "ptetaphim",
-                         mc_bins: Optional[int] = None) -> None:
-    """gvx_mass_histogram_peers: the fused histogram whose CTAs add their counts straight into
-    every peer's bins (``peer_bins_dev``: device address of an array of ``npeers`` device
-    pointers) or into one multicast address (``mc_bins``). The caller owns the cross-rank
-    barriers around the call (see allreduce_mass_histogram)."""
+                         mc_bins: Optional[int] = None, work: Optional[torch.Tensor] = None) -> None:
+    """gvx_mass_histogram_peers: the fused histogram whose CTAs pre-reduce into a device-local
+    workspace (``work``: int64[nbins+3], zero, left zero; default: one cached per device, nbins
+    and stream) and whose last CTA adds the totals into every peer's bins (``peer_bins_dev``:
+    device address of an array of ``npeers`` device pointers) or into one multicast address
+    (``mc_bins``). The caller owns the cross-rank barriers around the call (see
+    allreduce_mass_histogram)."""
     a, n, dt, dev, _ = _view(v1, 4, "v1")
     b, n2, dt2, dev2, _ = _view(v2, 4, "v2")
     if n != n2:
@@ -512,11 +526,15 @@ def mass_histogram_peers(v1: VecArg, v2: VecArg, peer_bins_dev: int, npeers: int
     if dt != dt2 or dev != dev2:
         raise ValueError("v1 and v2 must share dtype and device")
     mptr = _out_1d(m_out, n, dt, "m_out")
+    if work is None:
+        work = _peer_work(int(nbins), dev, _stream(dev))
+    elif work.dtype != torch.int64 or work.device != dev or work.numel() < nbins + 3 or not work.is_contiguous():
+        raise ValueError(f"work must be a contiguous int64 tensor of >= nbins+3 = {nbins + 3} on {dev}")
     with torch.cuda.device(dev):
         _check(lib.gvx_mass_histogram_peers(_dtype_code(dt), _coords_code(coords), ctypes.byref(a), ctypes.byref(b), n,
                                             float(lo), float(hi), int(nbins), int(peer_bins_dev) or None,
-                                            int(npeers), mc_bins, GVX_HIST_BOOST_TO_CM if cm else 0, mptr,
-                                            _stream(dev)), "gvx_mass_histogram_peers")
+                                            int(npeers), mc_bins, work.data_ptr(), GVX_HIST_BOOST_TO_CM if cm else 0,
+                                            mptr, _stream(dev)), "gvx_mass_histogram_peers")
 
 
 _SYMM_BINS = {}

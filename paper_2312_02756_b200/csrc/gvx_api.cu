@@ -964,31 +964,35 @@ static gvx_status mass_histogram_impl(gvx_dtype dtype, gvx_coords coords, const 
                                       const gvx_vec4_cview* v2, int64_t n, double lo, double hi, int32_t nbins,
                                       unsigned long long* bins, uint32_t flags, void* m_out,
                                       const gvx_vec4_view* boosted_out, gvx_stream_t stream,
-                                      unsigned long long* const* peers, int32_t npeers, unsigned long long* mc);
+                                      unsigned long long* const* peers, int32_t npeers, unsigned long long* mc,
+                                      unsigned long long* work);
 
 gvx_status gvx_mass_histogram(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1, const gvx_vec4_cview* v2,
                               int64_t n, double lo, double hi, int32_t nbins, unsigned long long* bins, uint32_t flags,
                               void* m_out, const gvx_vec4_view* boosted_out, gvx_stream_t stream) {
   return mass_histogram_impl(dtype, coords, v1, v2, n, lo, hi, nbins, bins, flags, m_out, boosted_out, stream,
-                             nullptr, 0, nullptr);
+                             nullptr, 0, nullptr, nullptr);
 }
 
 gvx_status gvx_mass_histogram_peers(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,
                                     const gvx_vec4_cview* v2, int64_t n, double lo, double hi, int32_t nbins,
                                     unsigned long long* const* peer_bins, int32_t npeers,
-                                    unsigned long long* mc_bins, uint32_t flags, void* m_out, gvx_stream_t stream) {
+                                    unsigned long long* mc_bins, unsigned long long* work, uint32_t flags,
+                                    void* m_out, gvx_stream_t stream) {
   if (mc_bins ? !aligned(mc_bins, 8) : (!peer_bins || !aligned(peer_bins, 8) || npeers < 1 || npeers > 4096))
     return GVX_ERR_INVALID_ARGUMENT;
-  // the kernels flush through the sink (HistParams peers / mc) and never touch a local `bins`
+  if (!work || !aligned(work, 8)) return GVX_ERR_INVALID_ARGUMENT;
+  // the kernels flush into `work`; each launch's last CTA pushes the totals to the sink
   return mass_histogram_impl(dtype, coords, v1, v2, n, lo, hi, nbins, nullptr, flags, m_out, nullptr, stream,
-                             mc_bins ? nullptr : peer_bins, mc_bins ? 0 : npeers, mc_bins);
+                             mc_bins ? nullptr : peer_bins, mc_bins ? 0 : npeers, mc_bins, work);
 }
 
 static gvx_status mass_histogram_impl(gvx_dtype dtype, gvx_coords coords, const gvx_vec4_cview* v1,
                                       const gvx_vec4_cview* v2, int64_t n, double lo, double hi, int32_t nbins,
                                       unsigned long long* bins, uint32_t flags, void* m_out,
                                       const gvx_vec4_view* boosted_out, gvx_stream_t stream,
-                                      unsigned long long* const* peers, int32_t npeers, unsigned long long* mc) {
+                                      unsigned long long* const* peers, int32_t npeers, unsigned long long* mc,
+                                      unsigned long long* work) {
   if (!valid_dtype(dtype) || !valid_coords(coords) || n < 0) return GVX_ERR_INVALID_ARGUMENT;
   if (nbins < 1 || nbins > (1 << 28) || !isfinite(lo) || !isfinite(hi) || !(lo < hi)) return GVX_ERR_INVALID_ARGUMENT;
   if ((flags & ~GVX_HIST_BOOST_TO_CM) != 0u) return GVX_ERR_INVALID_ARGUMENT;
@@ -1005,6 +1009,7 @@ static gvx_status mass_histogram_impl(gvx_dtype dtype, gvx_coords coords, const 
   hp.peers = peers;
   hp.npeers = npeers;
   hp.mc = mc;
+  hp.work = work;
   cudaStream_t s = (cudaStream_t)stream;
 #define GVX_HIST_DISPATCH(T, C)                                                                                  \
   (cm ? dispatch_hist<T, C, true>(v1, v2, n, hp, bins, m_out, boosted_out, s)                       \

@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(256, MINB) k_mass_histogram(View4<T> v1, View4
       if (c) hist_flush(bins, hp, b, c);
     }
   }
+  hist_tail(hp);  // pre-reduced cross-GPU sink only (gvx_mass_histogram_peers)
 }
 
 // ============================================================================
@@ -1226,6 +1227,7 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
         else atomicAdd(&co.bins[b - nb2], (unsigned long long)c);
       }
     }
+    hist_tail(hp);  // pre-reduced cross-GPU sink only (gvx_mass_histogram_peers)
   }
 }
 

@@ -839,6 +839,10 @@ struct HistParams {
   unsigned long long* const* peers;  // device array of npeers bin arrays, or NULL
   int npeers;
   unsigned long long* mc;            // multicast address of the bins (multimem.red), or NULL
+  // Pre-reduction for the peers / mc sink: CTAs flush into this device-local
+  // workspace (nbins+2 counters, then a ticket word); the last CTA of the launch
+  // pushes the <= nbins+2 non-zero totals to the sink and leaves it zeroed.
+  unsigned long long* work;
 };
 
 inline HistParams make_hist_params(double lo, double hi, int nbins) {
@@ -864,19 +868,50 @@ inline HistParams make_hist_params(double lo, double hi, int nbins) {
   hp.peers = nullptr;
   hp.npeers = 0;
   hp.mc = nullptr;
+  hp.work = nullptr;
   return hp;
 }
 
 // Add count c to bin b of the histogram described by hp (see HistParams).
-__device__ __forceinline__ void hist_flush(unsigned long long* bins, const HistParams& hp, int b,
-                                           unsigned long long c) {
+__device__ __forceinline__ void hist_push(const HistParams& hp, int b, unsigned long long c) {
   if (hp.mc) {
     asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(hp.mc + b), "l"(c) : "memory");
-  } else if (hp.npeers > 0) {
+  } else {
     for (int p = 0; p < hp.npeers; ++p) atomicAdd_system(hp.peers[p] + b, c);
+  }
+}
+__device__ __forceinline__ void hist_flush(unsigned long long* bins, const HistParams& hp, int b,
+                                           unsigned long long c) {
+  if (hp.work) {
+    atomicAdd(hp.work + b, c);  // device-local partial sum; hist_tail pushes the totals
+  } else if (hp.mc || hp.npeers > 0) {
+    hist_push(hp, b, c);
   } else {
     atomicAdd(bins + b, c);
   }
+}
+
+// Kernel tail of the pre-reduced cross-GPU sink (hp.work != NULL), reached by every
+// thread of every CTA after its last hist_flush: each thread fences its flush atomics,
+// one ticket per CTA is taken after a CTA barrier, and the CTA that takes the last
+// ticket reads-and-clears the workspace and pushes each non-zero total once to the
+// sink — <= nbins+2 remote adds per peer per launch (multimem.red: per launch)
+// instead of one per CTA and bin — then re-arms the ticket for the next launch.
+__device__ __forceinline__ void hist_tail(const HistParams& hp) {
+  if (!hp.work) return;  // uniform over the grid
+  __shared__ int is_last;
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(hp.work + hp.nbins + 2);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int b = threadIdx.x; b < hp.nbins + 2; b += blockDim.x) {
+    const unsigned long long c = atomicExch(hp.work + b, 0ull);
+    if (c) hist_push(hp, b, c);
+  }
+  if (threadIdx.x == 0) atomicExch(ticket, 0u);
 }
 
 __device__ __noinline__ int find_bin_exact(double x, const HistParams& hp) {

@@ -160,12 +160,15 @@ def test_mass_histogram_peers_validation(gvx):
     by = ctypes.byref
     a, b = _view(), _view()
     P = L.gvx_mass_histogram_peers
-    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, None, 2, None, 0, None, None) == 1     # no peers
-    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 0, None, 0, None, None) == 1   # npeers < 1
-    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, 0x4004, 2, None, 0, None, None) == 1   # misaligned
-    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, None, 0, 0x5001, 0, None, None) == 1   # misaligned mc
-    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 1.0, 1.0, 10, 0x4000, 2, None, 0, None, None) == 1   # bad axis
-    assert P(gvx.GVX_F64, 0, by(a), by(b), 0, 0.0, 1.0, 10, 0x4000, 2, None, 0, None, None) == 0   # n == 0
+    W = 0x6000  # an aligned (never dereferenced) workspace address
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, None, 2, None, W, 0, None, None) == 1     # no peers
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 0, None, W, 0, None, None) == 1   # npeers < 1
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, 0x4004, 2, None, W, 0, None, None) == 1   # misaligned
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, None, 0, 0x5001, W, 0, None, None) == 1   # misaligned mc
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 1.0, 1.0, 10, 0x4000, 2, None, W, 0, None, None) == 1   # bad axis
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 2, None, None, 0, None, None) == 1  # no work
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 4, 0.0, 1.0, 10, 0x4000, 2, None, W + 4, 0, None, None) == 1  # misaligned
+    assert P(gvx.GVX_F64, 0, by(a), by(b), 0, 0.0, 1.0, 10, 0x4000, 2, None, W, 0, None, None) == 0   # n == 0
 
 
 def test_dimuon_axis_limit(gvx):

@@ -932,6 +932,33 @@ def test_mass_histogram_peers_simulated(gvx, dt, cm):
         gvx.mass_histogram_peers(v1, v2, ptrs.data_ptr(), 0)
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_mass_histogram_peers_prereduce_workspace(gvx, dt):
+    """The pre-reduced sink: CTAs add into the caller's workspace and the last CTA of each launch
+    pushes the totals to the peers and clears it — so the workspace is all zero after every call
+    (and its ticket re-armed), and back-to-back calls of different sizes and paths (TMA ring,
+    register kernel, lab and CM) sharing one workspace each deliver exactly the plain histogram."""
+    import synth.device as sd
+    work = torch.zeros(gvx.DEFAULT_NBINS + 3, dtype=torch.int64, device="cuda")
+    peers = [gvx.new_bins() for _ in range(2)]
+    ptrs = torch.tensor([t.data_ptr() for t in peers], dtype=torch.int64, device="cuda")
+    for n in (1, 4097, 300_000, 3 * 1536 * 148 + 5):
+        v1, v2 = sd.muon_pairs(n, first=n, dtype=TDT[dt])
+        pr = torch.stack([v1, v2], 1).contiguous()
+        for a, b in ((v1, v2), (pr[:, 0], pr[:, 1])):
+            for cm in (False, True):
+                ref = gvx.mass_histogram(a, b, cm=cm)
+                for t in peers:
+                    t.zero_()
+                gvx.mass_histogram_peers(a, b, ptrs.data_ptr(), 2, cm=cm, work=work)
+                torch.cuda.synchronize()
+                assert int(work.abs().sum()) == 0, (n, cm)
+                for t in peers:
+                    assert torch.equal(t, ref), (n, cm)
+    with pytest.raises(ValueError):
+        gvx.mass_histogram_peers(v1, v2, ptrs.data_ptr(), 2, work=work[:10])
+
+
 def test_allreduce_mass_histogram_symmetric_memory_world1():
     """The symmetric-memory plumbing (rendezvous, peer pointer array, device barriers) on a
     one-rank NCCL group: the fused all-reduce equals the plain histogram."""
@@ -1298,3 +1325,29 @@ def test_mixed_coordinate_pair_closed_form(gvx):
     mc = torch.empty(5, dtype=torch.float64, device="cuda")
     gvx.mass_histogram(a, b, cm=True, coords="ptetaphim", coords2="pxpypze", m_out=mc)
     assert np.all(np.abs(host(mc) ** 2 - E * E) <= 1e-12 * E * E)
+
+
+def test_bench_two_ranks_self_check():
+    """bench.py's N > 1 path end to end on one GPU: two torchrun ranks (gloo, both mapped to
+    cuda:0 by GVX_BENCH_SAME_DEVICE — plumbing only, never numbers) shard the index space,
+    all-reduce the bins, and rank 0's self-check recomputes the one-GPU histogram of all global
+    indices: the line must report bins_equal and n_gpus 2."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "2",
+           "--warmup", "3", "--events", "1000003", "--dist-backend", "gloo", "--no-e2e", "--no-per-op"]
+    for extra in ([], ["--two-launch"]):
+        r = subprocess.run(cmd + extra, cwd=root, capture_output=True, text=True, timeout=900,
+                           env=dict(os.environ, GVX_BENCH_SAME_DEVICE="1", PYTHONPATH=root))
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+        line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+        assert line["n_gpus"] == 2 and line["self_check"]["bins_equal"], line.get("self_check")
+        assert line["self_check"]["events"] == 2 * 1000003
