@@ -736,6 +736,9 @@ def gpu_time(fn, reps, flush):
         # here, outside the timed region, and L2 is left holding clean lines (a write-flush would
         # leave 126 MB of dirty lines for the timed kernel to write back)
         flush.sum(dtype=torch.int32)
+        # keep the GPU busy (~50 us) while the host enqueues the timed launch, so the interval
+        # a -> b is the kernel on the device, not the Python/ctypes call that issues it
+        torch.cuda._sleep(100_000)
         a.record()
         fn()
         b.record()
