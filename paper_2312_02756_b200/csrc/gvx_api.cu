@@ -194,7 +194,7 @@ template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 1
 // fp64 lab histogram: 20 warps x 2 interleaved events, 0.904 vs 0.934 ms (same sweep)
 template <> struct TmaCfgOf<double, PM_HIST> { using type = PairTma<double, 1280, 2, 20, 1>; };
 template <> struct TmaCfgOf<double, PM_HIST_CM_COS> { using type = PairTma<double, 1536, 2, 24, 1>; };
-template <> struct TmaCfgOf<double, PM_BOTH> { using type = PairTma<double, 1536, 2, 24, 1>; };
+template <> struct TmaCfgOf<double, PM_BOTH> { using type = PairTma<double, 1536, 2, 24, 1, 80>; };
 template <int MODE> struct TmaCfgOf<float, MODE> { using type = PairTma<float, 896, 4, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM> { using type = PairTma<float, 1792, 3, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM_COS> { using type = PairTma<float, 1792, 3, 28, 1>; };
@@ -224,7 +224,7 @@ gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v
   const size_t sm = CFG::smem_bytes(nbs);
   if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
   auto k = soa ? k_pair_tma<T, C, MODE, CFG, false, true> : k_pair_tma<T, C, MODE, CFG, false, false>;
-  const int block = 32 * (CFG::NCW + 1);
+  const int block = CFG::THREADS;
   int per_sm = blocks_per_sm(k, block, sm);
   if (per_sm < 1) return GVX_ERR_UNSUPPORTED;
   const int64_t ntiles = n / CFG::TILE;
@@ -277,6 +277,11 @@ gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, i
       case 17: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1152, 3, 18, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       case 18: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1536, 2, 12, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       case 19: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1536, 2, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      // warp-specialised register split (setmaxnreg): producer warpgroup at 24, consumers at CREG
+      case 20: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1536, 2, 24, 1, 80>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 21: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1024, 3, 16, 1, 112>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 22: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1280, 2, 20, 1, 88>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 23: return launch_pair_tma_cfg<T, C, MODE, PairTma<double, 1280, 2, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       default: break;
     }
   }
@@ -290,6 +295,9 @@ gvx_status launch_pair_tma(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, i
       case 6: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1536, 4, 24, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       case 7: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1280, 5, 20, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       case 8: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1024, 6, 16, 1>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 9: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1792, 3, 28, 1, 64>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 10: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1536, 4, 24, 1, 72>>(v1, v2, n, m_out, hp, bins, bo, s, co);
+      case 11: return launch_pair_tma_cfg<T, C, MODE, PairTma<float, 1280, 4, 20, 1, 88>>(v1, v2, n, m_out, hp, bins, bo, s, co);
       default: break;
     }
   }
@@ -491,7 +499,7 @@ gvx_status launch_step(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64
   const size_t sm = (size_t)CFG::RING_BYTES + BR::RING_BYTES + 16 * (CFG::STAGES + BR::BST) + (size_t)nbs * 4;
   if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
   auto k = k_step<T, CFG, BR>;
-  const int block = 32 * (CFG::NCW + 1 + BR::NBW);
+  const int block = StepGeom<CFG, BR>::THREADS;
   if (blocks_per_sm(k, block, sm) < 1) return GVX_ERR_UNSUPPORTED;
   const int grid = sm_count();
   if (n > ((int64_t)grid << 31)) return GVX_ERR_UNSUPPORTED;  // per-CTA uint32 counters
@@ -910,7 +918,13 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
 #else
     const int c = 2;  // 18 pair warps + 6 boost warps (tools/step_probe.py: 2.62 vs 2.67-2.77 ms)
 #endif
-    if (c == 1)
+    if (c == 3)
+      st = launch_step<double, PairTma<double, 1280, 2, 20, 1, 80>, BoostRing<double, 256, 4, 4, 80>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 4)
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1, 88>, BoostRing<double, 512, 3, 8, 56>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 1)
       st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 512, 3, 8>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
     else if (c == 0)

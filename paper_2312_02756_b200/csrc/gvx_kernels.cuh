@@ -26,6 +26,14 @@ enum Coords { C_PTETAPHIM = 0, C_PXPYPZE = 1, C_PXPYPZM = 2, C_PTETAPHIE = 3 };
 enum PairMode { PM_MASS = 0, PM_HIST = 1, PM_HIST_CM = 2, PM_HIST_CM_COS = 3, PM_BOTH = 4 };
 
 template <typename T> struct View4 { const T* c[4]; int64_t s; };
+
+// Warpgroup register reallocation (sm_90a+): every warp of the warpgroup executes it.
+template <int R> __device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R));
+}
+template <int R> __device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R));
+}
 template <typename T> struct View4o { T* c[4]; int64_t s; };
 template <typename T> struct View3 { const T* c[3]; int64_t s; };
 
@@ -893,9 +901,20 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1))
 // bytes in flight are set by STAGES x TILE, not by register occupancy.
 // ============================================================================
 
-template <typename T, int TILE_, int STAGES_, int NCW_, int MINB_ = 1>
+// CREG > 0: warp-specialised register split (setmaxnreg): the producer is a whole
+// warpgroup (4 warps, lane 0 of warp 0 issues) shrunk to 24 registers, and the
+// consumer warps (NCW a multiple of 4) grow to CREG — registers move inside the
+// CTA's launch allocation, so 24 + NCW / 4 * CREG <= (NCW / 4 + 1) * the launch
+// count (static_assert below, with the launch count __launch_bounds__ allows).
+template <typename T, int TILE_, int STAGES_, int NCW_, int MINB_ = 1, int CREG_ = 0>
 struct PairTma {
-  static constexpr int TILE = TILE_, STAGES = STAGES_, NCW = NCW_, MINB = MINB_;
+  static constexpr int TILE = TILE_, STAGES = STAGES_, NCW = NCW_, MINB = MINB_, CREG = CREG_;
+  static constexpr int PW = CREG > 0 ? 4 : 1;                    // producer warps
+  static constexpr int THREADS = 32 * (NCW + PW);
+  static constexpr int PREG = 24;
+  static_assert(CREG == 0 || (NCW % 4 == 0 && MINB == 1 && CREG % 8 == 0 &&
+                              PREG + NCW / 4 * CREG <= (NCW / 4 + 1) * ((65536 / THREADS) / 8 * 8)),
+                "setmaxnreg budget");
   static constexpr int NCT = NCW * 32;
   static constexpr int EPT = TILE / NCT;
   static constexpr int VEC = 4 * (int)sizeof(T);                 // bytes per 4-vector
@@ -1096,7 +1115,7 @@ __device__ __forceinline__ void pair_consume_x2(const double (&a0)[4], const dou
 // SOA = true: the 8 component tiles of v1 and v2 (8 bulk copies), read back
 // lane-contiguously (LDS.64 / LDS.32, no bank conflicts).
 template <typename T, int COORDS, int MODE, typename CFG, bool WANT_BO = false, bool SOA = false>
-__global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(View4<T> v1, View4<T> v2,
+__global__ void __launch_bounds__(CFG::THREADS, CFG::MINB) k_pair_tma(View4<T> v1, View4<T> v2,
                                                                  int64_t n, T* __restrict__ m_out, HistParams hp,
                                                                  unsigned long long* __restrict__ bins, View4o<T> bo,
                                                                  CosOut<T> co) {
@@ -1125,8 +1144,9 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
 
   const int64_t ntiles = n / CFG::TILE;
   constexpr int TV = CFG::TILE * 4;  // scalars per array tile
-  if (warp == 0) {
-    if (lane == 0) {  // producer
+  if (warp < CFG::PW) {
+    if constexpr (CFG::CREG > 0) setmaxnreg_dec<CFG::PREG>();
+    if (warp == 0 && lane == 0) {  // producer
       const uint64_t pol = tma::policy_evict_first();
       int s = 0, it = 0;
       uint32_t ph = 1;  // parity of the empty-barrier phase to wait for (round k-1)
@@ -1144,15 +1164,21 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
             tma::bulk_g2s(dst + TV + c * CFG::TILE, v2.c[c] + t * CFG::TILE, CFG::HALF / 4, &full[s], pol);
           }
         } else {
-          tma::bulk_g2s(dst, v1.c[0] + t * TV, CFG::HALF, &full[s], pol);
-          tma::bulk_g2s(dst + TV, v2.c[0] + t * TV, CFG::HALF, &full[s], pol);
+#ifdef GVX_PROBE_L2_RESIDENT  // tools/probe only: every tile re-reads one of 64 (compute-bound control)
+          const int64_t tr = t & 63;
+#else
+          const int64_t tr = t;
+#endif
+          tma::bulk_g2s(dst, v1.c[0] + tr * TV, CFG::HALF, &full[s], pol);
+          tma::bulk_g2s(dst + TV, v2.c[0] + tr * TV, CFG::HALF, &full[s], pol);
         }
         ++it;
         if (++s == CFG::STAGES) { s = 0; ph ^= 1u; }
       }
     }
   } else {  // consumers
-    const int ctid = threadIdx.x - 32;
+    if constexpr (CFG::CREG > 0) setmaxnreg_inc<CFG::CREG>();
+    const int ctid = threadIdx.x - 32 * CFG::PW;
     int s = 0;
     uint32_t ph = 0;  // parity of the full-barrier phase of this round
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -1242,9 +1268,11 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1), CFG::MINB) k_pair_tma(Vie
 // (same arithmetic, same bits); warps NCW+1..NCW+NBW boost (boost_coef /
 // apply_boost as k_boost: same bits) and store with 256-bit STG.
 // ============================================================================
-template <typename T, int BT_, int BST_, int NBW_>
+// BREG: the boost warps' register count under the step's warp-specialised split
+// (the pair CFG has CREG > 0; the boost warps are then whole warpgroups too).
+template <typename T, int BT_, int BST_, int NBW_, int BREG_ = 0>
 struct BoostRing {
-  static constexpr int BT = BT_, BST = BST_, NBW = NBW_, NBT = NBW * 32;
+  static constexpr int BT = BT_, BST = BST_, NBW = NBW_, NBT = NBW * 32, BREG = BREG_;
   static constexpr int EPB = BT / NBT;              // boost events per thread per stage
   static constexpr int VB = BT * 4 * (int)sizeof(T);  // vector tile bytes
   static constexpr int BB = BT * 3 * (int)sizeof(T);  // velocity tile bytes
@@ -1253,8 +1281,24 @@ struct BoostRing {
   static_assert(BT % NBT == 0 && BB % 16 == 0 && VB % 16 == 0, "boost tile geometry");
 };
 
+template <typename CFG, typename BR>
+struct StepGeom {
+  static constexpr int PW = CFG::PW, THREADS = 32 * (CFG::PW + CFG::NCW + BR::NBW);
+  static constexpr int LAUNCH_REG = (65536 / THREADS) / 8 * 8;  // what __launch_bounds__(THREADS, 1) allows
+  static_assert(CFG::CREG == 0 ||
+                    (BR::NBW % 4 == 0 && BR::BREG % 8 == 0 && BR::BREG >= 24 &&
+                     CFG::PREG + CFG::NCW / 4 * CFG::CREG + BR::NBW / 4 * BR::BREG <= THREADS / 128 * LAUNCH_REG),
+                "setmaxnreg budget of the step");
+};
+
+template <int FROM, int TO>
+__device__ __forceinline__ void setmaxnreg_to() {
+  if constexpr (TO > FROM) setmaxnreg_inc<TO>();
+  if constexpr (TO < FROM) setmaxnreg_dec<TO>();
+}
+
 template <typename T, typename CFG, typename BR>
-__global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
+__global__ void __launch_bounds__(StepGeom<CFG, BR>::THREADS, 1)
     k_step(View4<T> v1, View4<T> v2, int64_t n, T* __restrict__ m_out, HistParams hp,
            unsigned long long* __restrict__ bins, CosOut<T> co, const T* __restrict__ bv, const T* __restrict__ bb,
            T* __restrict__ bout, int64_t nb) {
@@ -1286,8 +1330,10 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
 
   const int64_t ntiles = n / CFG::TILE, nbtiles = nb / BR::BT;
   constexpr int TV = CFG::TILE * 4;
-  if (warp == 0) {
-    if (lane == 0) {  // producer of both rings; never blocks on one while the other can move
+  using G = StepGeom<CFG, BR>;
+  if (warp < G::PW) {
+    if constexpr (CFG::CREG > 0) setmaxnreg_dec<CFG::PREG>();
+    if (warp == 0 && lane == 0) {  // producer of both rings; never blocks on one while the other can move
       const uint64_t pol = tma::policy_evict_first();
       int64_t t = blockIdx.x, tb = blockIdx.x;
       int s = 0, it = 0, bs = 0, bit = 0;
@@ -1317,8 +1363,9 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
         }
       }
     }
-  } else if (warp <= CFG::NCW) {  // pair consumers (the k_pair_tma PM_BOTH loop)
-    const int ctid = threadIdx.x - 32;
+  } else if (warp < G::PW + CFG::NCW) {  // pair consumers (the k_pair_tma PM_BOTH loop)
+    if constexpr (CFG::CREG > 0) setmaxnreg_to<G::LAUNCH_REG, CFG::CREG>();
+    const int ctid = threadIdx.x - 32 * G::PW;
     int s = 0;
     uint32_t ph = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -1351,7 +1398,8 @@ __global__ void __launch_bounds__(32 * (CFG::NCW + 1 + BR::NBW), 1)
       }
     }
   } else {  // boost warps
-    const int btid = threadIdx.x - 32 * (CFG::NCW + 1);
+    if constexpr (CFG::CREG > 0) setmaxnreg_to<G::LAUNCH_REG, BR::BREG>();
+    const int btid = threadIdx.x - 32 * (G::PW + CFG::NCW);
     View4o<T> o;
     o.c[0] = bout; o.c[1] = bout + 1; o.c[2] = bout + 2; o.c[3] = bout + 3; o.s = 4;
     int s = 0;

@@ -37,7 +37,9 @@ template <int R> __device__ __forceinline__ void reg_inc() { asm volatile("setma
 template <int R> __device__ __forceinline__ void reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R)); }
 
 // (B) warp-specialised: warpgroup 0 = producer (warp 0 lane 0 issues), warpgroups 1..NCWG consume.
-template <int NCWG, int CREG, int PREG, int TILE, int STAGES>
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int NCWG, int CREG, int PREG, int TILE, int STAGES, int WAIT = 0>
 __global__ void __launch_bounds__(128 * (NCWG + 1), 1)
     k_ws(View4<double> v1, View4<double> v2, int64_t n, double* __restrict__ m_out, HistParams hp,
          unsigned long long* __restrict__ bins, View4o<double>, CosOut<double> co) {
@@ -72,8 +74,9 @@ __global__ void __launch_bounds__(128 * (NCWG + 1), 1)
         if (it >= STAGES) { tma::mbar_wait(&empty[s], ph); tma::fence_proxy_async_smem(); }
         tma::mbar_arrive_expect_tx(&full[s], 2 * HALF);
         double* dst = ring + (size_t)s * 2 * TV;
-        tma::bulk_g2s(dst, v1.c[0] + t * TV, HALF, &full[s], pol);
-        tma::bulk_g2s(dst + TV, v2.c[0] + t * TV, HALF, &full[s], pol);
+        const int64_t ts = WAIT == 2 ? (t & 63) : t;  // WAIT 2: every tile re-reads one of 64 (L2-resident)
+        tma::bulk_g2s(dst, v1.c[0] + ts * TV, HALF, &full[s], WAIT == 2 ? 0 : pol);
+        tma::bulk_g2s(dst + TV, v2.c[0] + ts * TV, HALF, &full[s], WAIT == 2 ? 0 : pol);
         ++it;
         if (++s == STAGES) { s = 0; ph ^= 1u; }
       }
@@ -84,7 +87,13 @@ __global__ void __launch_bounds__(128 * (NCWG + 1), 1)
     int s = 0;
     uint32_t ph = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      tma::mbar_wait(&full[s], ph);
+      if constexpr (WAIT != 1) {
+        tma::mbar_wait(&full[s], ph);
+      } else {  // one consumer warp polls the mbarrier, the others sleep in a named barrier
+        if (warp == 4) tma::mbar_wait(&full[s], ph);
+        named_bar_sync(1, NCT);
+        if (warp != 4) while (!tma::mbar_try_wait(&full[s], ph)) {}
+      }
       const double* src = ring + (size_t)s * 2 * TV;
       double a[EPT][4], b[EPT][4];
 #pragma unroll
@@ -197,6 +206,11 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   }
 }
 
+__global__ void cvt(const double* s, float* d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = (float)s[i];
+}
+
 struct Ctx {
   double *v1, *v2, *m;
   int64_t n;
@@ -249,6 +263,44 @@ int main(int argc, char** argv) {
   Ctx c;
   c.n = argc > 1 ? atoll(argv[1]) : 100000000LL;
   const bool only_product = argc > 2 && argv[2][0] == 'p';
+  if (argc > 2 && argv[2][0] == 'f') {  // f32 product fused pass only (ncu capture)
+    CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, 0));
+    float *f1, *f2, *fm;
+    unsigned long long* fb;
+    CK(cudaMalloc(&f1, c.n * 16));
+    CK(cudaMalloc(&f2, c.n * 16));
+    CK(cudaMalloc(&fm, c.n * 4));
+    CK(cudaMalloc(&fb, 2 * 1002 * 8));
+    double* tmp;
+    CK(cudaMalloc(&tmp, (c.n / 4 + 1) * 32));
+    for (int which = 0; which < 2; ++which)
+      for (int64_t o = 0; o < c.n; o += c.n / 4 + 1) {
+        const int64_t k = std::min<int64_t>(c.n / 4 + 1, c.n - o);
+        gen<<<4 * c.sms, 256>>>(tmp, k, 11 + which * 7 + o);
+        cvt<<<4 * c.sms, 256>>>(tmp, (which ? f2 : f1) + 4 * o, 4 * k);
+      }
+    CK(cudaDeviceSynchronize());
+    CK(cudaEventCreate(&c.e0));
+    CK(cudaEventCreate(&c.e1));
+    c.hp = make_hist_params(0.25, 300.0, 1000);
+    using CFG = PairTma<float, 1792, 3, 28, 1>;
+    auto k = k_pair_tma<float, C_PTETAPHIM, PM_BOTH, CFG, false, false>;
+    const size_t smem = CFG::smem_bytes(2004);
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    View4<float> a{{f1, f1 + 1, f1 + 2, f1 + 3}, 4}, b{{f2, f2 + 1, f2 + 2, f2 + 3}, 4};
+    CosOut<float> co{make_hist_params(0.25, 300.0, 1000), fb + 1002, nullptr};
+    for (int r = 0; r < 5; ++r) {
+      CK(cudaEventRecord(c.e0));
+      k<<<c.sms, CFG::THREADS, smem>>>(a, b, c.n, fm, c.hp, fb, View4o<float>{}, co);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(c.e1));
+      CK(cudaEventSynchronize(c.e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, c.e0, c.e1));
+      printf("f32 k_pair_tma PM_BOTH 1792x3x28: %.4f ms\n", ms);
+    }
+    return 0;
+  }
   CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, 0));
   CK(cudaMalloc(&c.v1, c.n * 32));
   CK(cudaMalloc(&c.v2, c.n * 32));
@@ -264,15 +316,24 @@ int main(int argc, char** argv) {
   const size_t hist = 2 * 1002 * 4;
   {
     using CFG = PairTma<double, 1536, 2, 24, 1>;
-    run(c, "product k_pair_tma 1536x2x24", k_pair_tma<double, C_PTETAPHIM, PM_BOTH, CFG, false, false>, 32 * 25,
+    run(c, "k_pair_tma 1536x2x24", k_pair_tma<double, C_PTETAPHIM, PM_BOTH, CFG, false, false>, CFG::THREADS,
+        CFG::smem_bytes(2004), 1);
+  }
+  {
+    using CFG = PairTma<double, 1536, 2, 24, 1, 80>;
+    run(c, "k_pair_tma 1536x2x24 ws c80", k_pair_tma<double, C_PTETAPHIM, PM_BOTH, CFG, false, false>, CFG::THREADS,
         CFG::smem_bytes(2004), 1);
   }
   if (only_product) return 0;
-#define WS(NCWG, CREG, PREG, TILE, ST)                                                                      \
-  run(c, "ws " #NCWG "wg c" #CREG " p" #PREG " " #TILE "x" #ST,                                           \
-      k_ws<NCWG, CREG, PREG, TILE, ST>, 128 * (NCWG + 1), (size_t)ST * TILE * 64 + ST * 16 + hist, 1)
-  WS(4, 112, 24, 1024, 3);
-  WS(3, 152, 24, 768, 4);
+#define WS(NCWG, CREG, PREG, TILE, ST, W)                                                                      \
+  run(c, "ws " #NCWG "wg c" #CREG " p" #PREG " " #TILE "x" #ST " wait" #W,                                 \
+      k_ws<NCWG, CREG, PREG, TILE, ST, W>, 128 * (NCWG + 1), (size_t)ST * TILE * 64 + ST * 16 + hist, 1)
+  WS(6, 80, 24, 1536, 2, 0);
+  WS(6, 80, 24, 1536, 2, 2);
+  WS(6, 80, 24, 1536, 2, 1);
+  WS(4, 112, 24, 1024, 3, 0);
+  WS(4, 112, 24, 1024, 3, 1);
+  if (argc > 2 && argv[2][0] == 'w') return 0;
 #define SELF(NW, S, EPT, MINB)                                                                          \
   run(c, "self " #NW "w s" #S " ept" #EPT " minb" #MINB, k_self<NW, S, EPT, MINB>, 32 * NW,             \
       (size_t)NW * S * 64 * 32 * EPT + NW * S * 8 + hist, MINB)
