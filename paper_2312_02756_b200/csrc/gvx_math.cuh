@@ -133,14 +133,16 @@ __device__ __forceinline__ double add_exponent(double x, int k) {
   return __hiloint2double(__double2hiint(x) + (k << 20), __double2loint(x));
 }
 
-// k = rint(x * c) with the 1.5*2^52 shifter, valid for |x c| < 2^51: one DFMA
-// (x c + MAGIC, rounded once: the nearest integer to the exact product) lands
-// the integer in the low word, one DADD recovers it as a double. Replaces a DMUL
-// and FRND.F64 / F2I.F64, which run on the narrow XU pipe (ncu showed it
-// oversubscribed).
-__device__ __forceinline__ double rint_mul(double x, double c, int& ki) {
+// Round to nearest integer with the 1.5*2^52 shifter, valid for |v| < 2^51:
+// the integer lands in the low word of v + MAGIC. Replaces FRND.F64 and
+// F2I.F64, which run on the narrow XU pipe (ncu showed it oversubscribed).
+// (Folding the product into one DFMA, fma(x, c, MAGIC), saves a DP op per call
+// but costs registers: MAGIC then needs a register pair. Measured in round 2:
+// the SoA f64 mass kernel went 128 -> 133 registers, one CTA per SM, 1.07 ->
+// 1.37 ms; so the multiply stays separate.)
+__device__ __forceinline__ double rint_shift(double v, int& ki) {
   const double MAGIC = 6755399441055744.0;  // 1.5 * 2^52
-  double t = __fma_rn(x, c, MAGIC);
+  double t = __dadd_rn(v, MAGIC);
   ki = __double2loint(t);
   return __dsub_rn(t, MAGIC);
 }
@@ -150,7 +152,7 @@ __device__ __forceinline__ double rint_mul(double x, double c, int& ki) {
 // (near-minimax degree 10 / 11: error <= 2.2e-16 relative).
 __device__ __forceinline__ void sinh_cosh(double x, double& sh, double& ch) {
   int ki;
-  double k = rint_mul(x, kCoef[K_LOG2E], ki);
+  double k = rint_shift(x * kCoef[K_LOG2E], ki);
   double r = fma(-k, kCoef[K_LN2_HI], x);
   r = fma(-k, kCoef[K_LN2_LO], r);
   double s = r * r;
@@ -190,7 +192,7 @@ __device__ __forceinline__ double neg_if(double x, int q) {
 // sin and cos of x, |x| <= 2048: x = k pi/2 + r, |r| <= pi/4 (+ulp).
 __device__ __forceinline__ void fast_sincos(double x, double& sn, double& cs) {
   int q;
-  double k = rint_mul(x, kCoef[K_2_PI], q);
+  double k = rint_shift(x * kCoef[K_2_PI], q);
   double r = fma(-k, kCoef[K_PIO2_HI], x);  // exact for |k| < 2^11
   r = fma(-k, kCoef[K_PIO2_LO], r);
   double s, c;
@@ -206,7 +208,7 @@ __device__ __forceinline__ void fast_sincos(double x, double& sn, double& cs) {
 // degree-16 even near-minimax polynomial — no quadrant selects.
 __device__ __forceinline__ double fast_cos(double x) {
   int ki;
-  double k = rint_mul(x, kCoef[K_INV_PI], ki);
+  double k = rint_shift(x * kCoef[K_INV_PI], ki);
   double r = fma(-k, kCoef[K_PI_HI], x);  // exact for |k| < 2^10
   r = fma(-k, kCoef[K_PI_LO], r);
   double z = r * r;
@@ -292,16 +294,12 @@ __device__ __forceinline__ T energy_of(T m, T q);
 // and the fused lab + CM pass:
 //   M^2 = t1 + t2 + 2 (E1 E2 - pt1 pt2 (c + sh1 sh2)),  t = m|m| (E^2 - |p|^2),
 // or t = -q^2 for a clamped vector (E^2 < 0 -> E = 0, reading R2).
-__device__ __noinline__ double clamped_masses(double q1, double mm1, bool c1, double q2, double mm2, bool c2) {
-  return (c1 ? -(q1 * q1) : mm1) + (c2 ? -(q2 * q2) : mm2);
-}
 __device__ __forceinline__ double pair_mass_from(double pt1, double m1, double pt2, double m2, double c, double sh1,
                                                  double sh2, double q1, double q2, double E1, double E2) {
   double mm1 = m1 * fabs(m1), mm2 = m2 * fabs(m2);
   // clamp test on the sign bit of E^2 (integer op; E^2 = -0 is impossible: q >= pt > 0)
   bool c1 = __double2hiint(fma(q1, q1, mm1)) < 0, c2 = __double2hiint(fma(q2, q2, mm2)) < 0;
-  double t = mm1 + mm2;
-  if (c1 | c2) t = clamped_masses(q1, mm1, c1, q2, mm2, c2);  // rare: a clamped vector (R2)
+  double t = (c1 ? -(q1 * q1) : mm1) + (c2 ? -(q2 * q2) : mm2);
   double m2sq = t + 2.0 * (E1 * E2 - pt1 * pt2 * (c + sh1 * sh2));
   return copy_sign_bit(fast_sqrt_abs(m2sq), m2sq);
 }
