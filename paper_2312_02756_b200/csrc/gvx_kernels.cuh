@@ -551,20 +551,45 @@ __global__ void __launch_bounds__(256) k_mixed_pairs(View4<T> v1, View4<T> v2, i
 // One thread per event, grid-stride: the offsets reads are coalesced, the
 // muon reads of consecutive events are contiguous (256-bit AoS loads).
 // ============================================================================
+// Scattered gathers (the jagged kernels' charges and muon rows): loads with a 64-B
+// L2 prefetch size. By default an L2 miss of such a load fetches a 128-B segment
+// from DRAM, so a selected event's 64 B of f64 muons cost ~2.1 segments' worth;
+// with .L2::64B they cost 1.5 (tools/probe/gatherprobe.cu: 2.35 -> 1.42 GB of DRAM
+// reads for 0.96 GB of 64-B records at random rows).
+__device__ __forceinline__ void ld_gather(const double* p, double (&r)[4]) {
+  asm("ld.global.nc.L1::no_allocate.L2::64B.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld_gather(const float* p, float (&r)[4]) {
+  asm("ld.global.nc.L1::no_allocate.L2::64B.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]) : "l"(p));
+}
+__device__ __forceinline__ double ld_gather1(const double* p) {
+  double r;
+  asm("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_gather1(const float* p) {
+  float r;
+  asm("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int32_t ld_gather1(const int32_t* p) {
+  int32_t r;
+  asm("ld.global.nc.L2::64B.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
 template <typename T, bool AOS>
 __device__ __forceinline__ void load_muon(const View4<T>& mu, int64_t j, T (&x)[4]) {
   if constexpr (AOS) {
-    if constexpr (sizeof(T) == 8) {
-      double r[4];
-      ld256(reinterpret_cast<const double*>(mu.c[0]) + 4 * j, r);
+    T r[4];
+    ld_gather(mu.c[0] + 4 * j, r);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) x[c] = (T)r[c];
-    } else {
-      float4 r = __ldg(reinterpret_cast<const float4*>(mu.c[0]) + j);
-      x[0] = r.x; x[1] = r.y; x[2] = r.z; x[3] = r.w;
-    }
+    for (int c = 0; c < 4; ++c) x[c] = r[c];
   } else {
-    load_event(mu, j, x);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = ld_gather1(mu.c[c] + j * mu.s);
   }
 }
 
@@ -685,8 +710,8 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_compact(View4<T> mu, const 
       two[k] = el < ne && s_off[el + 1] - s_off[el] == 2;
       qa[k] = qb[k] = 0;
       if (two[k]) {
-        qa[k] = __ldg(q + s_off[el]);
-        qb[k] = __ldg(q + s_off[el] + 1);
+        qa[k] = ld_gather1(q + s_off[el]);
+        qb[k] = ld_gather1(q + s_off[el] + 1);
       }
     }
 #pragma unroll
