@@ -20,6 +20,7 @@ METRICS = [
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
+    ("dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "DRAM read % of peak"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
     ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU pipe %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
@@ -66,8 +67,9 @@ def main():
     lines = [f"# ncu --set full summary ({dtype}, N = {n:.0e} events per launch)", "",
              f"Source: `{os.path.basename(rep)}` (captured on a B200 under gpurun with "
              "`--clock-control none`; per-launch replays are cold-cache and serialised).", "",
-             "| kernel | " + " | ".join(lbl for _, lbl in METRICS) + " | algorithmic bytes | DRAM/algorithmic |",
-             "|" + "---|" * (len(METRICS) + 3)]
+             "| kernel | " + " | ".join(lbl for _, lbl in METRICS) + " | algorithmic bytes | DRAM/algorithmic "
+             "| DRAM GB/s (bytes / duration) |",
+             "|" + "---|" * (len(METRICS) + 4)]
     traffic = {}
     for r in rows[2:]:
         if len(r) < len(h):
@@ -94,7 +96,10 @@ def main():
 
         dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
         ab = algo.get(key, 0) * n
-        lines.append(f"| `{key}` ({name[:60]}) | " + " | ".join(vals) + f" | {ab:.3e} | {dram / ab if ab else 0:.3f} |")
+        dur = num("gpu__time_duration.sum") * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3,
+                                                "ms": 1e-3, "nsecond": 1e-9}.get(units[h.index("gpu__time_duration.sum")], 1e-9)
+        lines.append(f"| `{key}` ({name[:60]}) | " + " | ".join(vals) + f" | {ab:.3e} | {dram / ab if ab else 0:.3f} "
+                     f"| {dram / dur / 1e9:.0f} |")
         traffic[key] = {"dram_bytes_per_launch": dram, "algorithmic_bytes_per_launch": ab, "events_per_launch": n,
                         "dram_bytes_per_event": dram / n, "kernel": name[:120]}
     os.makedirs(rdir, exist_ok=True)
