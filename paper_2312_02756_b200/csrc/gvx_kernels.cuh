@@ -714,16 +714,47 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_compact(View4<T> mu, const 
         qb[k] = ld_gather1(q + s_off[el] + 1);
       }
     }
+    if constexpr (sizeof(T) == 4) {
+      // f32: compaction once per thread, not once per event — the thread's selected
+      // events as a bit mask, a warp-inclusive scan of the counts (5 shuffles), one
+      // shared atomic per warp for the warp's block of the list (the per-event ballot,
+      // leader atomic and broadcast below cost ~45 instructions per event). 0.542 ->
+      // 0.524 ms at 1e8. For f64 it measured slower (0.664 -> 0.788 ms: more spills
+      // under the 48-register cap that 5 CTAs/SM need), so f64 keeps the per-event form.
+      unsigned int mask = 0u;
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const int el = tid + k * NT;
-      const bool sel = two[k] && (int64_t)qa[k] * (int64_t)qb[k] < 0;
-      const unsigned int bal = __ballot_sync(0xffffffffu, sel);
+      for (int k = 0; k < EPT; ++k) {
+        const int el = tid + k * NT;
+        // q0 q1 < 0 (the oracle's 64-bit product, R21) <=> opposite signs, neither zero
+        const bool sel = two[k] & ((qa[k] ^ qb[k]) < 0) & (qa[k] != 0) & (qb[k] != 0);
+        mask |= (unsigned int)sel << k;
+        if (!sel && m_out && el < ne) m_out[e0 + el] = T(NAN);
+      }
+      const int cnt = __popc(mask);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
       int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(&s_n, __popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (sel) s_list[base + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)el;
-      else if (m_out && el < ne) m_out[e0 + el] = T(NAN);
+      if (lane == 31 && incl) base = atomicAdd(&s_n, incl);
+      base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k)
+        if (mask & (1u << k)) s_list[base++] = (uint16_t)(tid + k * NT);
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const int el = tid + k * NT;
+        const bool sel = two[k] && (int64_t)qa[k] * (int64_t)qb[k] < 0;
+        const unsigned int bal = __ballot_sync(0xffffffffu, sel);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&s_n, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (sel) s_list[base + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)el;
+        else if (m_out && el < ne) m_out[e0 + el] = T(NAN);
+      }
     }
     __syncthreads();
     const int n = s_n;

@@ -571,6 +571,16 @@ def test_dimuon_histogram_parity(gvx, O, dt):
     mb = torch.empty(boff.size - 1, dtype=TDT[dt], device="cuda")
     hb = host(gvx.dimuon_histogram(dev(big), dev(bq), dev(boff), m_out=mb))
     assert int(hb.sum()) == sel_b and np.array_equal(np.isnan(host(mb)), np.isnan(mb_o))
+    # charges beyond +-1 (R21 selects on the sign of the 64-bit product q0 q1): zero, large
+    # magnitudes and the int32 extremes, whose 32-bit product would overflow
+    rng = np.random.default_rng(5)
+    qx = rng.choice(np.array([0, 1, -1, 7, -7, 1 << 30, -(1 << 30), 2**31 - 1, -2**31], np.int64),
+                    size=q.size).astype(np.int32)
+    hx_o, mx_o, sel_x = O.dimuon_histogram(mu, qx, off, LO, HI, NB)
+    mx = torch.empty(off.size - 1, dtype=TDT[dt], device="cuda")
+    hx = host(gvx.dimuon_histogram(tm, dev(qx), to, m_out=mx))
+    assert int(hx.sum()) == sel_x and np.array_equal(np.isnan(host(mx)), np.isnan(mx_o))
+    assert sel_x > 1000 and sel_x != sel
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
