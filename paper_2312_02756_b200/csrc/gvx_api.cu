@@ -935,6 +935,32 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
     if (st != GVX_ERR_UNSUPPORTED) return st;
   }
+#ifdef GVX_TUNE
+  // Tuning build only: the f32 step in one launch (GVX_STEP32_CFG = 1..4), for A/B runs.
+  const int c32 = tune_env("GVX_STEP32_CFG");
+  if (c32 && dtype == GVX_F32 && n >= (int64_t(1) << 20) && nb >= (int64_t(1) << 20) && coords == GVX_PTETAPHIM &&
+      tma_enabled() && classify(v1, es) == L_AOS && classify(v2, es) == L_AOS && aos4(bv, es) &&
+      aos3(beta, es) && aos4(bout, es) && aligned(bout->c[0], 4 * es)) {
+    const HistParams hp = make_hist_params(lo, hi, nbins);
+    const float* pv = (const float*)bv->c[0];
+    const float* pb = (const float*)beta->c[0];
+    float* po = (float*)bout->c[0];
+    gvx_status st = GVX_ERR_UNSUPPORTED;
+    if (c32 == 1)
+      st = launch_step<float, PairTma<float, 1536, 3, 24, 1>, BoostRing<float, 512, 3, 4>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 2)
+      st = launch_step<float, PairTma<float, 1280, 3, 20, 1>, BoostRing<float, 768, 3, 8>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 3)
+      st = launch_step<float, PairTma<float, 1536, 3, 24, 1, 64>, BoostRing<float, 512, 3, 4, 56>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 4)
+      st = launch_step<float, PairTma<float, 1280, 3, 20, 1, 72>, BoostRing<float, 768, 3, 8, 56>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    if (st != GVX_ERR_UNSUPPORTED) return st;
+  }
+#endif
   // any other shape: the two calls it fuses (same bits)
   gvx_status st = n > 0 ? gvx_pair_histograms(dtype, coords, v1, v2, n, lo, hi, nbins, lab_bins, cm_bins, m_out,
                                               cm_m_out, stream)

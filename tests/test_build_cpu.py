@@ -39,7 +39,7 @@ def test_warp_specialised_kernels_launch_with_the_assumed_registers():
                 continue
             ncw = int(p.group(3))
             warps = 4 + ncw
-            b = re.search(r"BoostRing<double, (\d+), (\d+), (\d+)(?:, (\d+))?>", name)
+            b = re.search(r"BoostRing<(?:double|float), (\d+), (\d+), (\d+)(?:, (\d+))?>", name)
             if "k_step" in name and b:
                 warps += int(b.group(3))
             want = (65536 // (32 * warps)) // 8 * 8
