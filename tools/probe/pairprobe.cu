@@ -211,6 +211,113 @@ __global__ void cvt(const double* s, float* d, int64_t n) {
     d[i] = (float)s[i];
 }
 
+
+// x3: three events per thread in one branch-free block (PM_BOTH, fast domain), else one by one.
+__device__ __forceinline__ void consume3(const double (&a)[3][4], const double (&b)[3][4], const int64_t (&i)[3],
+                                         double* __restrict__ m_out, unsigned int* sh_hist, const HistParams& hp,
+                                         unsigned int* sh_cos, const CosOut<double>& co) {
+  bool ok = true;
+#pragma unroll
+  for (int u = 0; u < 3; ++u) ok = ok & fast_domain(a[u][0], a[u][1], a[u][2], a[u][3]) & fast_domain(b[u][0], b[u][1], b[u][2], b[u][3]);
+  if (ok) {
+    double M[3], C[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      both_masses_fast(a[u][0], a[u][1], a[u][2], a[u][3], b[u][0], b[u][1], b[u][2], b[u][3], M[u], C[u]);
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      atomicAdd(&sh_hist[find_bin(M[u], hp)], 1u);
+      atomicAdd(&sh_cos[find_bin(C[u], co.hc)], 1u);
+      if (m_out) m_out[i[u]] = M[u];
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      pair_consume<double, C_PTETAPHIM, PM_BOTH, false>(a[u], b[u], i[u], m_out, sh_hist, hp, View4o<double>{}, sh_cos, co);
+  }
+}
+
+template <int NCWG, int CREG, int TILE, int STAGES>
+__global__ void __launch_bounds__(128 * (NCWG + 1), 1)
+    k_ws3(View4<double> v1, View4<double> v2, int64_t n, double* __restrict__ m_out, HistParams hp,
+          unsigned long long* __restrict__ bins, View4o<double>, CosOut<double> co) {
+  constexpr int NCW = 4 * NCWG, NCT = NCW * 32, EPT = TILE / NCT, HALF = TILE * 32, TV = TILE * 4;
+  constexpr int RING = STAGES * 2 * HALF;
+  static_assert(TILE == 3 * NCT, "three events per thread");
+  constexpr int RL = (65536 / (128 * (NCWG + 1))) / 8 * 8;
+  static_assert(24 + NCWG * CREG <= RL * (NCWG + 1), "setmaxnreg budget");
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING);
+  uint64_t* empty = full + STAGES;
+  unsigned int* sh_hist = reinterpret_cast<unsigned int*>(empty + STAGES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb2 = hp.nbins + 2, nbt = nb2 + co.hc.nbins + 2;
+  unsigned int* sh_cos = sh_hist + nb2;
+  for (int b = threadIdx.x; b < nbt; b += blockDim.x) sh_hist[b] = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { tma::mbar_init(&full[s], 1); tma::mbar_init(&empty[s], NCW); }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t ntiles = n / TILE;
+  if (warp < 4) {
+    reg_dec<24>();
+    if (warp == 0 && lane == 0) {
+      const uint64_t pol = tma::policy_evict_first();
+      int s = 0, it = 0;
+      uint32_t ph = 1;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (it >= STAGES) { tma::mbar_wait(&empty[s], ph); tma::fence_proxy_async_smem(); }
+        tma::mbar_arrive_expect_tx(&full[s], 2 * HALF);
+        double* dst = ring + (size_t)s * 2 * TV;
+        tma::bulk_g2s(dst, v1.c[0] + t * TV, HALF, &full[s], pol);
+        tma::bulk_g2s(dst + TV, v2.c[0] + t * TV, HALF, &full[s], pol);
+        ++it;
+        if (++s == STAGES) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else {
+    reg_inc<CREG>();
+    const int ctid = threadIdx.x - 128;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      tma::mbar_wait(&full[s], ph);
+      const double* src = ring + (size_t)s * 2 * TV;
+      double a[3][4], b[3][4];
+      int64_t idx[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int e = u * NCT + ctid;
+        lds_vec(src, e, lane, a[u]);
+        lds_vec(src + TV, e, lane, b[u]);
+        idx[u] = t * TILE + e;
+      }
+      tma::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[s]);
+      consume3(a, b, idx, m_out, sh_hist, hp, sh_cos, co);
+      if (++s == STAGES) { s = 0; ph ^= 1u; }
+    }
+    if (blockIdx.x == gridDim.x - 1) {
+      for (int64_t i = ntiles * TILE + ctid; i < n; i += NCT) {
+        double a[4], b[4];
+        for (int c = 0; c < 4; ++c) { a[c] = v1.c[0][4 * i + c]; b[c] = v2.c[0][4 * i + c]; }
+        pair_consume<double, C_PTETAPHIM, PM_BOTH, false>(a, b, i, m_out, sh_hist, hp, View4o<double>{}, sh_cos, co);
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbt; b += blockDim.x) {
+    unsigned int c = sh_hist[b];
+    if (c) {
+      if (b < nb2) atomicAdd(&bins[b], (unsigned long long)c);
+      else atomicAdd(&co.bins[b - nb2], (unsigned long long)c);
+    }
+  }
+}
+
 struct Ctx {
   double *v1, *v2, *m;
   int64_t n;
@@ -334,6 +441,16 @@ int main(int argc, char** argv) {
   WS(4, 112, 24, 1024, 3, 0);
   WS(4, 112, 24, 1024, 3, 1);
   if (argc > 2 && argv[2][0] == 'w') return 0;
+  if (argc > 2 && argv[2][0] == '3') {
+#define WS3(NCWG, CREG, TILE, ST)                                                                        \
+  run(c, "x3 " #NCWG "wg c" #CREG " " #TILE "x" #ST, k_ws3<NCWG, CREG, TILE, ST>, 128 * (NCWG + 1),      \
+      (size_t)ST * TILE * 64 + ST * 16 + hist, 1)
+    WS3(4, 112, 1536, 2);
+    WS3(3, 152, 1152, 3);
+    WS3(5, 88, 1920, 1);
+    WS3(4, 112, 1536, 2);
+    return 0;
+  }
 #define SELF(NW, S, EPT, MINB)                                                                          \
   run(c, "self " #NW "w s" #S " ept" #EPT " minb" #MINB, k_self<NW, S, EPT, MINB>, 32 * NW,             \
       (size_t)NW * S * 64 * 32 * EPT + NW * S * 8 + hist, MINB)
