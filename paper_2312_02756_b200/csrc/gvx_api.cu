@@ -662,12 +662,53 @@ gvx_status launch_dimuon_compact(const gvx_vec4_cview* mu, const int32_t* q, con
   return e == cudaSuccess ? GVX_OK : cuda_fail(e);
 }
 
-// GVX_DIMUON_IMPL=tma / ldg selects the streaming kernels for A/B runs.
+// Carried-list dimuon kernel (default): ET events per tile, NT threads, CPS CTAs
+// per SM (tools/probe/dimuon3.cu sweep: f64 512 / 128 / 8, f32 1024 / 256 / 5 with
+// __launch_bounds__ min 4 — the f32 kernel compiled for min 5 CTAs got 40
+// registers and ran 0.72 ms instead of 0.48 at the same 5 CTAs per SM).
+template <typename T, bool AOS, bool WANT_M, bool VOFF>
+gvx_status launch_dimuon_carry(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
+                               const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
+  constexpr bool F64 = sizeof(T) == 8;
+  constexpr int ET = F64 ? 512 : 1024, NT = F64 ? 128 : 256, MINB = F64 ? 8 : 4, CPS = F64 ? 8 : 5;
+  const size_t sm = DimuonCarry<ET, NT>::smem(hp.nbins + 2, WANT_M);
+  if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
+  auto k = k_dimuon_carry<T, AOS, ET, NT, MINB, WANT_M, VOFF>;
+  int per_sm = blocks_per_sm(k, NT, sm);
+  if (per_sm < 1) return GVX_ERR_UNSUPPORTED;
+  if (per_sm > CPS) per_sm = CPS;
+  const int64_t ntiles = (n_events + ET - 1) / ET;
+  const int64_t full = (int64_t)sm_count() * per_sm;
+  const int grid = (int)(ntiles < full ? ntiles : full);
+  // uint32 shared-memory bins: one launch covers at most grid * 2^31 events
+  // (a multiple of 4 events, so a chunk's offsets keep the 32-byte alignment)
+  const int64_t chunk = (int64_t)grid << 31;
+  for (int64_t o = 0; o < n_events; o += chunk) {
+    const int64_t cn = n_events - o < chunk ? n_events - o : chunk;
+    k<<<grid, NT, sm, s>>>(mk4<T>(mu), q, off + o, cn, hp, bins, m_out ? (T*)m_out + o : nullptr);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GVX_OK : cuda_fail(e);
+}
+
+template <typename T, bool AOS>
+gvx_status launch_dimuon_carry(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
+                               const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
+  const bool voff = aligned(off, 32);
+  if (m_out)
+    return voff ? launch_dimuon_carry<T, AOS, true, true>(mu, q, off, n_events, hp, bins, m_out, s)
+                : launch_dimuon_carry<T, AOS, true, false>(mu, q, off, n_events, hp, bins, m_out, s);
+  return voff ? launch_dimuon_carry<T, AOS, false, true>(mu, q, off, n_events, hp, bins, m_out, s)
+              : launch_dimuon_carry<T, AOS, false, false>(mu, q, off, n_events, hp, bins, m_out, s);
+}
+
+// GVX_DIMUON_IMPL=tma / ldg / compact selects the other kernels for A/B runs.
 int dimuon_impl() {
   static const int v = [] {
     const char* e = getenv("GVX_DIMUON_IMPL");
     if (e && e[0] == 't') return 1;
     if (e && e[0] == 'l') return 2;
+    if (e && e[0] == 'c') return 3;
     return 0;
   }();
   return v;
@@ -681,8 +722,13 @@ gvx_status launch_dimuon(const gvx_vec4_cview* mu, const int32_t* q, const int64
   for (int k = 1; k < 4; ++k) aos = aos && (const char*)mu->c[k] == b + k * sizeof(T);
   const size_t nb2 = (size_t)hp.nbins + 2;
   if (nb2 > kMaxSmemBins) return GVX_ERR_UNSUPPORTED;
+  const bool aos_vec = aos && aligned(b, sizeof(T) == 8 ? 32 : 16);  // 256-bit (f64) / 128-bit (f32) muon loads
   if (dimuon_impl() == 0) {
-    const bool aos_vec = aos && aligned(b, sizeof(T) == 8 ? 32 : 16);  // 256-bit (f64) / 128-bit (f32) muon loads
+    gvx_status st = aos_vec ? launch_dimuon_carry<T, true>(mu, q, off, n_events, hp, bins, m_out, s)
+                            : launch_dimuon_carry<T, false>(mu, q, off, n_events, hp, bins, m_out, s);
+    if (st != GVX_ERR_UNSUPPORTED) return st;
+  }
+  if (dimuon_impl() == 3) {
     gvx_status st = aos_vec ? launch_dimuon_compact<T, true>(mu, q, off, n_events, hp, bins, m_out, s)
                             : launch_dimuon_compact<T, false>(mu, q, off, n_events, hp, bins, m_out, s);
     if (st != GVX_ERR_UNSUPPORTED) return st;

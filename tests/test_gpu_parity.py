@@ -584,6 +584,55 @@ def test_dimuon_histogram_parity(gvx, O, dt):
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_dimuon_carried_list_edges(gvx, O, dt):
+    """The default dimuon kernel (k_dimuon_carry: consecutive-event selection, a circular
+    list carried across tiles, L2 prefetch) against the oracle on the shapes that stress
+    its bookkeeping: batches below / at / just above one tile (512 f64, 1024 f32 events)
+    and with a ragged last tile, every event selected (the list at its 2 ET + NT bound),
+    none selected, offsets that are 8- but not 32-byte aligned (the scalar offset loads),
+    with and without m_out (the same bins)."""
+    mu, q, off = synth.jagged_events(0, 70_001, seed=31, dtype=dt)
+    for n in (1, 3, 511, 512, 513, 1023, 1024, 1025, 2049, 9_999, 70_001):
+        o = off[: n + 1]
+        h_o, m_o, sel = O.dimuon_histogram(mu, q, o, LO, HI, NB)
+        m_out = torch.empty(n, dtype=TDT[dt], device="cuda")
+        h = host(gvx.dimuon_histogram(dev(mu), dev(q), dev(o), m_out=m_out))
+        mg = host(m_out)
+        assert int(h.sum()) == sel and np.array_equal(np.isnan(mg), np.isnan(m_o)), n
+        ok = ~np.isnan(m_o)
+        if ok.any():
+            first = o[:-1][ok]
+            _, e = O.invariant_mass(mu[first], mu[first + 1])
+            assert mass_violations(mg[ok], m_o[ok], e, tau_of(dt)).size == 0, n
+            fails, _ = hist_check(h, m_o[ok], e, tau_of(dt), LO, HI, NB)
+            assert not fails, (n, fails)
+        assert np.array_equal(host(gvx.dimuon_histogram(dev(mu), dev(q), dev(o))), h), n
+    # offsets starting at event 1 (8-byte aligned, not 32): the same events, shifted
+    to = dev(off)
+    for s0 in (1, 2, 3):
+        sub = to[s0:]
+        h_o, _, sel = O.dimuon_histogram(mu, q, off[s0:], LO, HI, NB)
+        h = host(gvx.dimuon_histogram(dev(mu), dev(q), sub))
+        assert int(h.sum()) == sel
+        assert np.array_equal(h, host(gvx.dimuon_histogram(dev(mu), dev(q), dev(off[s0:].copy()))))
+    # every event a selected pair (list at capacity), then no event selected
+    n = 20_000
+    pm = mu[:2 * n].copy()  # event i owns rows 2i, 2i + 1
+    qa = np.tile(np.array([1, -1], np.int32), n)
+    oa = np.arange(0, 2 * n + 1, 2, dtype=np.int64)
+    h_o, m_o, sel = O.dimuon_histogram(pm, qa, oa, LO, HI, NB)
+    assert sel == n
+    m_out = torch.empty(n, dtype=TDT[dt], device="cuda")
+    h = host(gvx.dimuon_histogram(dev(pm), dev(qa), dev(oa), m_out=m_out))
+    _, e = O.invariant_mass(pm[0::2], pm[1::2])
+    assert int(h.sum()) == n and mass_violations(host(m_out), m_o, e, tau_of(dt)).size == 0
+    fails, _ = hist_check(h, m_o, e, tau_of(dt), LO, HI, NB)
+    assert not fails, fails
+    h = host(gvx.dimuon_histogram(dev(pm), dev(np.ones(2 * n, np.int32)), dev(oa), m_out=m_out))
+    assert int(h.sum()) == 0 and bool(torch.isnan(m_out).all())
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
 def test_lorentz_transform_parity(gvx, O, dt):
     v, beta = synth.boost_inputs(np.arange(200_003), dtype=dt, seed=23)
     b = (0.3, -0.4, 0.5)
