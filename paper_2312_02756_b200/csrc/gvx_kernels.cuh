@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_carry(View4<T> mu, const in
   constexpr int EPT = ET / NT;
   constexpr int CAP = DimuonCarry<ET, NT>::CAP;
   static_assert(ET % NT == 0 && EPT % 4 == 0 && EPT <= 32, "tile geometry");
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   int64_t* s_mo = reinterpret_cast<int64_t*>(smem);              // muon offset of each list entry
   int64_t* s_ev = s_mo + CAP;                                      // its event (WANT_M only)
   unsigned int* s_hist = reinterpret_cast<unsigned int*>(s_mo + (WANT_M ? 2 * CAP : CAP));
@@ -1211,10 +1211,11 @@ __device__ __forceinline__ void pair_consume_x2(const float (&a0)[4], const floa
     if constexpr (MODE == PM_BOTH) {
       M = pair_mass_f32_lanes<float2>(A0, A1, A2, A3, B0, B1, B2, B3);
       const float2 C = cm_mass_f32_lanes<float2, false, false>(A0, A1, A2, A3, B0, B1, B2, B3, &c, nullptr);
-      atomicAdd(&sh_hist[find_bin(M.x, hp)], 1u);
-      atomicAdd(&sh_hist[find_bin(M.y, hp)], 1u);
-      atomicAdd(&sh_cos[find_bin(C.x, co.hc)], 1u);
-      atomicAdd(&sh_cos[find_bin(C.y, co.hc)], 1u);
+      const int2 bm = find_bin2(M, hp), bc = find_bin2(C, co.hc);
+      atomicAdd(&sh_hist[bm.x], 1u);
+      atomicAdd(&sh_hist[bm.y], 1u);
+      atomicAdd(&sh_cos[bc.x], 1u);
+      atomicAdd(&sh_cos[bc.y], 1u);
       if (m_out) {
         m_out[i0] = M.x;
         m_out[i1] = M.y;
@@ -1234,15 +1235,17 @@ __device__ __forceinline__ void pair_consume_x2(const float (&a0)[4], const floa
     } else {
       M = cm_mass_f32_lanes<float2, COS, false>(A0, A1, A2, A3, B0, B1, B2, B3, &c, nullptr);
     }
-    atomicAdd(&sh_hist[find_bin(M.x, hp)], 1u);
-    atomicAdd(&sh_hist[find_bin(M.y, hp)], 1u);
+    const int2 bm = find_bin2(M, hp);
+    atomicAdd(&sh_hist[bm.x], 1u);
+    atomicAdd(&sh_hist[bm.y], 1u);
     if (m_out) {
       m_out[i0] = M.x;
       m_out[i1] = M.y;
     }
     if constexpr (COS) {
-      atomicAdd(&sh_cos[find_bin(c.x, co.hc)], 1u);
-      atomicAdd(&sh_cos[find_bin(c.y, co.hc)], 1u);
+      const int2 bc = find_bin2(c, co.hc);
+      atomicAdd(&sh_cos[bc.x], 1u);
+      atomicAdd(&sh_cos[bc.y], 1u);
       if (co.cos_out) {
         co.cos_out[i0] = c.x;
         co.cos_out[i1] = c.y;

@@ -653,6 +653,12 @@ __device__ __forceinline__ float2 lv_fma(float2 a, float2 b, float2 c) {
   return d;
 }
 __device__ __forceinline__ float2 lv_splat(float2, float x) { return make_float2(x, x); }
+// sign(v) sqrt(|v|) with ONE MUFU.SQRT and the sign bit copied by an integer op
+// (v >= 0 ? sqrt(v) : -sqrt(-v) compiled to two predicated MUFUs and an FADD;
+// same bits, -0 -> -0, NaN -> NaN).
+__device__ __forceinline__ float sqrt_abs_signed(float v) {
+  return __int_as_float(__float_as_int(fast_sqrt(fabsf(v))) | (__float_as_int(v) & (int)0x80000000));
+}
 template <typename F> __device__ __forceinline__ float lv_map(float a, F f) { return f(a); }
 template <typename F> __device__ __forceinline__ float2 lv_map(float2 a, F f) { return make_float2(f(a.x), f(a.y)); }
 template <typename F> __device__ __forceinline__ float lv_map2(float a, float b, F f) { return f(a, b); }
@@ -691,7 +697,7 @@ __device__ __forceinline__ V pair_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V 
   V y = lv_mul(lv_mul(pt1, pt2), inner);
   V x = lv_fma(E1, E2, lv_mul(y, MONE));
   V m2sq = lv_fma(x, TWO, t);
-  return lv_map(m2sq, [](float v) { return v >= 0.f ? fast_sqrt(v) : -fast_sqrt(-v); });
+  return lv_map(m2sq, [](float v) { return sqrt_abs_signed(v); });
 }
 
 // vec_out (WANT_VEC): the boosted pair in the rotated frame, (a2x, a2y, a2z, a2t, b2x, b2y, b2z, b2t).
@@ -758,7 +764,7 @@ __device__ __forceinline__ V cm_mass_f32_lanes(V pt1, V eta1, V phi1, V m1, V pt
                         return y;
                       }));
   }
-  return lv_map(m2sq, [](float x) { return x >= 0.f ? fast_sqrt(x) : -fast_sqrt(-x); });
+  return lv_map(m2sq, [](float x) { return sqrt_abs_signed(x); });
 }
 
 // ---------------------------------------------------------------------------
@@ -931,17 +937,33 @@ __device__ __forceinline__ int find_bin(double x, const HistParams& hp);
 // decides every event whose q is more than near_f from an integer, the rest (and
 // non-finite x) take the double path. Saves the F2F.F64 (XU) and the DP ops in the
 // issue-bound fp32 kernels.
+// The integer part of find_bin(float): q = (x - lo_f) scale_f, t = q + 1.5*2^23,
+// d = q - (t - 1.5*2^23) (all FP32, round to nearest).
+__device__ __forceinline__ int find_bin_f32_tail(float x, float q, float t, float d, const HistParams& hp) {
+  const int k = __float_as_int(t) - 0x4B400000;
+  const bool in = (unsigned)k <= (unsigned)hp.nbins;
+  int bin = in ? 1 + k - (__float_as_int(d) < 0 ? 1 : 0) : (__float_as_int(q) < 0 ? 0 : hp.nbins + 1);
+  if ((in & (fabsf(d) <= hp.near_f)) | ((__float_as_int(x) & 0x7fffffff) >= 0x7f800000)) bin = find_bin_exact((double)x, hp);
+  return bin;
+}
 __device__ __forceinline__ int find_bin(float x, const HistParams& hp) {
   if (!hp.f32_ok) return find_bin((double)x, hp);
   const float MAGIC = 12582912.f;  // 1.5 * 2^23
   const float q = __fmul_rn(__fsub_rn(x, hp.lo_f), hp.scale_f);
   const float t = __fadd_rn(q, MAGIC);
-  const int k = __float_as_int(t) - 0x4B400000;
   const float d = __fsub_rn(q, __fsub_rn(t, MAGIC));
-  const bool in = (unsigned)k <= (unsigned)hp.nbins;
-  int bin = in ? 1 + k - (__float_as_int(d) < 0 ? 1 : 0) : (__float_as_int(q) < 0 ? 0 : hp.nbins + 1);
-  if ((in & (fabsf(d) <= hp.near_f)) | ((__float_as_int(x) & 0x7fffffff) >= 0x7f800000)) bin = find_bin_exact((double)x, hp);
-  return bin;
+  return find_bin_f32_tail(x, q, t, d, hp);
+}
+// Two fp32 values (two events' masses) with the FP32 steps in packed FADD2 /
+// FMUL2 / FFMA2: the same roundings as find_bin(float) (x - lo = x + (-lo),
+// q - u = fma(u, -1, q)), so the same bins.
+__device__ __forceinline__ int2 find_bin2(float2 x, const HistParams& hp) {
+  if (!hp.f32_ok) return make_int2(find_bin((double)x.x, hp), find_bin((double)x.y, hp));
+  const float MAGIC = 12582912.f;
+  const float2 q = lv_mul(lv_add(x, lv_splat(x, -hp.lo_f)), lv_splat(x, hp.scale_f));
+  const float2 t = lv_add(q, lv_splat(x, MAGIC));
+  const float2 d = lv_fma(lv_add(t, lv_splat(x, -MAGIC)), lv_splat(x, -1.f), q);
+  return make_int2(find_bin_f32_tail(x.x, q.x, t.x, d.x, hp), find_bin_f32_tail(x.y, q.y, t.y, d.y, hp));
 }
 
 __device__ __forceinline__ int find_bin(double x, const HistParams& hp) {
