@@ -2,7 +2,8 @@
 """Summarise `ncu --set full` captures of the hot-path kernels into
 profiles/<round>/ncu_summary_<dtype>.md and profiles/ncu_traffic.json.
 
-Usage: python tools/ncu_summary.py <dtype> <report.ncu-rep> <round-dir> [n_events]
+Usage: python tools/ncu_summary.py <dtype> <report.ncu-rep>[,<report2.ncu-rep>...] <round-dir> [n_events]
+(several reports: one capture per gpurun call when a single one would exceed gpurun_out's size cap)
 
 ncu_traffic.json maps dtype -> bench kernel name -> DRAM bytes per launch
 (dram__bytes_read.sum + dram__bytes_write.sum) and the algorithmic bytes of the
@@ -61,17 +62,28 @@ def main():
     es = 8 if dtype == "f64" else 4
     algo = {"invariant_mass": 9 * es, "boost": 11 * es, "mass_histogram": 8 * es, "mass_histogram_cm": 8 * es,
             "cm_costheta_hist": 8 * es, "pairs": 9 * es, "step": 20 * es}
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
-    h, units = rows[0], rows[1]
+    reps = rep.split(",")
+    missing = [r for r in reps if not os.path.exists(r)]
+    if missing:
+        sys.exit(f"missing report(s): {missing}")  # never overwrite the summary / traffic with nothing
+    rows, h = [], None  # rows: (values, units) aligned to the first report's columns
+    for rp in reps:
+        out = subprocess.run(["ncu", "-i", rp, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rr = list(csv.reader(out.splitlines()))
+        if h is None:
+            h = rr[0]
+        hh, uu = rr[0], dict(zip(rr[0], rr[1]))
+        for r in rr[2:]:
+            d = dict(zip(hh, r))
+            rows.append(([d.get(k, "") for k in h], [uu.get(k, "") for k in h]))
     lines = [f"# ncu --set full summary ({dtype}, N = {n:.0e} events per launch)", "",
-             f"Source: `{os.path.basename(rep)}` (captured on a B200 under gpurun with "
+             f"Source: `{', '.join(os.path.basename(r) for r in reps)}` (captured on a B200 under gpurun with "
              "`--clock-control none`; per-launch replays are cold-cache and serialised).", "",
              "| kernel | " + " | ".join(lbl for _, lbl in METRICS) + " | algorithmic bytes | DRAM/algorithmic "
              "| DRAM GB/s (bytes / duration) |",
              "|" + "---|" * (len(METRICS) + 4)]
     traffic = {}
-    for r in rows[2:]:
+    for r, units in rows:
         if len(r) < len(h):
             continue
         name = r[h.index("Kernel Name")]

@@ -4,6 +4,8 @@
 #   bash tools/refresh_profiles.sh bench     # bench lines, launch list, widened rows, CFG2 sweep
 #   bash tools/refresh_profiles.sh ncu f64   # ncu --set full of every step kernel (then tools/ncu_summary.py)
 #   bash tools/refresh_profiles.sh ncu f32
+#   bash tools/refresh_profiles.sh ncu f64 "k_step|k_boost" a   # a subset per call (report suffix a) when one
+#   bash tools/refresh_profiles.sh ncu f64 "k_pair_tma" b       # report would exceed gpurun_out's 64 MiB cap
 set -x
 mkdir -p gpurun_out
 if [ "$1" = bench ]; then
@@ -16,6 +18,7 @@ if [ "$1" = bench ]; then
   python bench.py --sweep --sweep-out gpurun_out/nsweep_cfg2.jsonl > gpurun_out/sweep.log 2>> gpurun_out/refresh.err
 elif [ "$1" = ncu ]; then
   dt=${2:-f64}
-  ncu --set full --import-source on --clock-control none -k regex:"k_step|k_pair_tma|k_boost|k_invariant_mass|k_mass_histogram|k_cm_costheta" \
-      -f -o gpurun_out/prof_$dt python tools/prof_step.py --dtype $dt > gpurun_out/prof_$dt.log 2>&1
+  kre=${3:-"k_step|k_pair_tma|k_boost|k_invariant_mass|k_mass_histogram|k_cm_costheta"}
+  ncu --set full --import-source on --clock-control none -k regex:"$kre" \
+      -f -o gpurun_out/prof_$dt$4 python tools/prof_step.py --dtype $dt > gpurun_out/prof_$dt$4.log 2>&1
 fi
