@@ -52,6 +52,8 @@ LORENTZ_DEMO = [[_c, -_s, 0, 0], [_s, _c, 0, 0], [0, 0, _g, _g * 0.6], [0, 0, _g
 
 
 def one_launch_step(args) -> bool:
+    if getattr(args, "one_launch", False):
+        return True  # f32 too (the library takes one launch there only in the tuning build, GVX_STEP32_CFG)
     return args.dtype == "f64" and not getattr(args, "two_launch", False) and not getattr(args, "unfused", False)
 
 
@@ -70,6 +72,8 @@ def parse():
     p.add_argument("--dist-backend", default="nccl", help="process-group backend for N>1 (nccl on B200s)")
     p.add_argument("--two-launch", action="store_true",
                    help="f64: time the fused pair pass and the boost as two launches instead of one")
+    p.add_argument("--one-launch", action="store_true",
+                   help="time the step through gvx_pair_histograms_boost whatever the dtype (f32 A/B runs)")
     p.add_argument("--unfused", action="store_true",
                    help="time the step as four kernels (mass, boost, lab histogram, CM histogram) instead of the "
                         "fused pair pass + boost")

@@ -232,7 +232,9 @@ gvx_status launch_pair_tma_cfg(const gvx_vec4_cview* v1, const gvx_vec4_cview* v
   int grid = (int)(ntiles < 1 ? 1 : (ntiles < full ? ntiles : full));
   View4o<T> bov = mk4o<T>(bo);
   // Per-CTA uint32 counters: one launch covers at most grid * 2^31 events.
-  const int64_t chunk = MODE == PM_MASS ? n : ((int64_t)grid << 31);
+  int64_t chunk = MODE == PM_MASS ? n : ((int64_t)grid << 31);
+  const int64_t max_chunk = (int64_t)INT32_MAX * CFG::TILE;  // the kernel counts tiles in 32 bits
+  if (chunk > max_chunk) chunk = max_chunk;
   for (int64_t off = 0; off < n; off += chunk) {
     int64_t cn = n - off < chunk ? n - off : chunk;
     View4o<T> bo2 = bov;
@@ -503,6 +505,7 @@ gvx_status launch_step(const gvx_vec4_cview* v1, const gvx_vec4_cview* v2, int64
   if (blocks_per_sm(k, block, sm) < 1) return GVX_ERR_UNSUPPORTED;
   const int grid = sm_count();
   if (n > ((int64_t)grid << 31)) return GVX_ERR_UNSUPPORTED;  // per-CTA uint32 counters
+  if (nb / BR::BT >= INT32_MAX) return GVX_ERR_UNSUPPORTED;      // the kernel counts tiles in 32 bits
   CosOut<T> co{hp, cm_bins, (T*)cm_m_out};
   co.hc.peers = nullptr;
   co.hc.npeers = 0;

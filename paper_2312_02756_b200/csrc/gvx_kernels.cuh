@@ -1393,7 +1393,11 @@ __global__ void __launch_bounds__(CFG::THREADS, CFG::MINB) k_pair_tma(View4<T> v
     const int ctid = threadIdx.x - 32 * CFG::PW;
     int s = 0;
     uint32_t ph = 0;  // parity of the full-barrier phase of this round
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // 32-bit tile counter (the launchers keep n / TILE < 2^31): a 64-bit bound spilled to local
+    // memory and was reloaded every pass (ncu: LDL + long-scoreboard stall on the loop test)
+    const int ntiles32 = (int)ntiles;
+    for (int t32 = blockIdx.x; t32 < ntiles32; t32 += gridDim.x) {
+      const int64_t t = t32;
       tma::mbar_wait(&full[s], ph);
       const T* src = ring + (size_t)s * 2 * TV;
       T a[CFG::EPT][4], b[CFG::EPT][4];
@@ -1580,6 +1584,7 @@ __global__ void __launch_bounds__(StepGeom<CFG, BR>::THREADS, 1)
     const int ctid = threadIdx.x - 32 * G::PW;
     int s = 0;
     uint32_t ph = 0;
+    // (64-bit tile counter here: the 32-bit one measured 0.6 % slower for this kernel)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       tma::mbar_wait(&full[s], ph);
       const T* src = ring + (size_t)s * 2 * TV;
