@@ -666,14 +666,14 @@ gvx_status launch_dimuon_compact(const gvx_vec4_cview* mu, const int32_t* q, con
 }
 
 // Carried-list dimuon kernel (default): ET events per tile, NT threads, CPS CTAs
-// per SM (tools/probe/dimuon3.cu sweep: f64 512 / 128 / 8, f32 1024 / 256 / 5 with
-// __launch_bounds__ min 4 — the f32 kernel compiled for min 5 CTAs got 40
-// registers and ran 0.72 ms instead of 0.48 at the same 5 CTAs per SM).
+// per SM (tools/probe/dimuon3.cu sweeps, 32-bit list entries: f64 1024 / 128 / 8
+// 0.457 ms, f32 2048 / 256 / 4 0.392 ms; the f32 kernel is compiled for a minimum
+// of 4 CTAs: compiled for 5 it got 40 registers and ran 0.72 ms instead of 0.48).
 template <typename T, bool AOS, bool WANT_M, bool VOFF>
 gvx_status launch_dimuon_carry(const gvx_vec4_cview* mu, const int32_t* q, const int64_t* off, int64_t n_events,
                                const HistParams& hp, unsigned long long* bins, void* m_out, cudaStream_t s) {
   constexpr bool F64 = sizeof(T) == 8;
-  constexpr int ET = F64 ? 512 : 1024, NT = F64 ? 128 : 256, MINB = F64 ? 8 : 4, CPS = F64 ? 8 : 5;
+  constexpr int ET = F64 ? 1024 : 2048, NT = F64 ? 128 : 256, MINB = F64 ? 8 : 4, CPS = F64 ? 8 : 4;
   const size_t sm = DimuonCarry<ET, NT>::smem(hp.nbins + 2, WANT_M);
   if (sm > 227 * 1024) return GVX_ERR_UNSUPPORTED;
   auto k = k_dimuon_carry<T, AOS, ET, NT, MINB, WANT_M, VOFF>;

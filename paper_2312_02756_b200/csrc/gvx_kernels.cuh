@@ -797,8 +797,8 @@ constexpr size_t dimuon_compact_smem(int nb2) {
 // Jagged dimuon with a carried compaction list and an L2 prefetch pipeline
 // (default since round 2; k_dimuon_compact above is kept for A/B runs).
 // Measured against k_dimuon_compact (tools/probe/dimuon3.cu, 1e8 events):
-// f64 0.660 -> 0.510 ms, f32 0.520 -> 0.479 ms, bins bit-equal. Per CTA tile
-// of ET events:
+// f64 0.660 -> 0.46 ms, f32 0.50 -> 0.39 ms, bins bit-equal. Per CTA tile of
+// ET events:
 //   A. select: thread t takes EPT CONSECUTIVE events, so their EPT+1 offsets
 //      are EPT/4 256-bit loads and their charges a narrow window of the charge
 //      column (L1 hits for neighbouring events); q0 q1 < 0 (the 64-bit product
@@ -810,14 +810,22 @@ constexpr size_t dimuon_compact_smem(int nb2) {
 // The memory system runs ahead of both: thread NT-1 bulk-prefetches
 // (cp.async.bulk.prefetch.L2) the offsets of the CTA's tile two steps ahead
 // and the charge range of the next tile, so phase A reads L2, not DRAM.
-// The list holds <= (NT - 1) carried + 2 ET entries: CAP = next power of two.
+// The list holds <= (NT - 1) carried + 2 ET entries (CAP: the next power of
+// two). Entries are 32-bit muon offsets relative to offsets[0] when the
+// launch's muons span < 2^32 (the common case: half the shared memory of
+// 64-bit entries, which leaves L1 room for the charge window — f64 0.507 ->
+// 0.457 ms, f32 0.454 -> 0.398 ms in the probe); otherwise the same code runs
+// with 64-bit entries on half-size tiles in the same shared memory (a uniform
+// branch on offsets[n] - offsets[0], read by every CTA). The event of an entry
+// (for m_out) is packed as (CTA step << log2 ET) | event-in-tile in 32 bits.
 // ============================================================================
 template <int ET, int NT>
 struct DimuonCarry {
   static constexpr int need = 2 * ET + NT;
-  static constexpr int CAP = need <= 1024 ? 1024 : need <= 2048 ? 2048 : need <= 4096 ? 4096 : 8192;
-  static_assert(need <= 8192, "list capacity");
-  static constexpr size_t smem(int nb2, bool want_m) { return (size_t)CAP * 8 * (want_m ? 2 : 1) + (size_t)nb2 * 4; }
+  static constexpr int CAP = need <= 1024 ? 1024 : need <= 2048 ? 2048 : need <= 4096 ? 4096 : need <= 8192 ? 8192 : 16384;
+  static_assert(need <= 16384, "list capacity");
+  // 32-bit entries at ET (+ 32-bit events for m_out); the 64-bit fallback at ET / 2 fits the same bytes
+  static constexpr size_t smem(int nb2, bool want_m) { return (size_t)CAP * 4 * (want_m ? 2 : 1) + (size_t)nb2 * 4; }
 };
 
 // L2 bulk prefetch of the 16-byte granules covering [a, b) (at most 64 KB: a
@@ -831,24 +839,20 @@ __device__ __forceinline__ void prefetch_l2_range(const void* a, const void* b) 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
 }
 
-// VOFF: offsets 32-byte aligned (full tiles take 256-bit offset loads).
-template <typename T, bool AOS, int ET, int NT, int MINB, bool WANT_M, bool VOFF>
-__global__ void __launch_bounds__(NT, MINB) k_dimuon_carry(View4<T> mu, const int32_t* __restrict__ q,
-                                                      const int64_t* __restrict__ offsets, int64_t n_events,
-                                                      HistParams hp, unsigned long long* __restrict__ bins,
-                                                      T* __restrict__ m_out) {
+// The tile loop of k_dimuon_carry with list entries of type LT (uint32_t: muon
+// offset - mbase; int64_t: the muon offset itself, mbase = 0).
+template <typename T, bool AOS, int ET, int NT, bool WANT_M, bool VOFF, typename LT>
+__device__ __forceinline__ void dimuon_carry_tiles(const View4<T>& mu, const int32_t* __restrict__ q,
+                                                   const int64_t* __restrict__ offsets, int64_t n_events,
+                                                   const HistParams& hp, unsigned int* s_hist, unsigned char* smem,
+                                                   int* s_tail, T* __restrict__ m_out, int64_t mbase) {
   constexpr int EPT = ET / NT;
   constexpr int CAP = DimuonCarry<ET, NT>::CAP;
-  static_assert(ET % NT == 0 && EPT % 4 == 0 && EPT <= 32, "tile geometry");
-  extern __shared__ __align__(128) unsigned char smem[];
-  int64_t* s_mo = reinterpret_cast<int64_t*>(smem);              // muon offset of each list entry
-  int64_t* s_ev = s_mo + CAP;                                      // its event (WANT_M only)
-  unsigned int* s_hist = reinterpret_cast<unsigned int*>(s_mo + (WANT_M ? 2 * CAP : CAP));
-  __shared__ int s_tail;
-  const int nb2 = hp.nbins + 2;
+  constexpr int LOG2ET = ET == 256 ? 8 : ET == 512 ? 9 : ET == 1024 ? 10 : ET == 2048 ? 11 : 12;
+  static_assert(ET % NT == 0 && EPT % 4 == 0 && EPT <= 32 && (1 << LOG2ET) == ET, "tile geometry");
+  LT* s_mo = reinterpret_cast<LT*>(smem);                          // muon offset of each list entry
+  uint32_t* s_ev = reinterpret_cast<uint32_t*>(s_mo + CAP);         // its event, packed (WANT_M only)
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int b = tid; b < nb2; b += NT) s_hist[b] = 0u;
-  if (tid == 0) s_tail = 0;
   const int64_t ntiles = (n_events + ET - 1) / ET;
   const int64_t G = gridDim.x;
   auto tile_events = [&](int64_t t) { return n_events - t * ET < ET ? n_events - t * ET : (int64_t)ET; };
@@ -858,7 +862,8 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_carry(View4<T> mu, const in
   }
   __syncthreads();
   int head = 0, mark = 0;  // mark: the list tail before this iteration's selection
-  for (int64_t tile = blockIdx.x;; tile += G) {
+  uint32_t step = 0;       // this CTA's tile count (the packed event index of m_out)
+  for (int64_t tile = blockIdx.x;; tile += G, ++step) {
     const bool have = tile < ntiles;
     if (have) {
       // ---- A: select this tile's events, append them to the list
@@ -903,14 +908,14 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_carry(View4<T> mu, const in
         if (lane >= d) incl += v;
       }
       int base = 0;
-      if (lane == 31 && incl) base = atomicAdd(&s_tail, incl);
+      if (lane == 31 && incl) base = atomicAdd(s_tail, incl);
       base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
 #pragma unroll
       for (int k = 0; k < EPT; ++k)
         if (mask & (1u << k)) {
           const int slot = base++ & (CAP - 1);
-          s_mo[slot] = o[k];
-          if (WANT_M) s_ev[slot] = e0 + lb + k;
+          s_mo[slot] = (LT)(o[k] - mbase);
+          if (WANT_M) s_ev[slot] = (step << LOG2ET) | (uint32_t)(lb + k);
         }
       if (tid == NT - 1) {  // prefetch: the next tile's charges, the offsets two tiles ahead
         const int64_t t1 = tile + G, t2 = tile + 2 * G;
@@ -921,26 +926,52 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_carry(View4<T> mu, const in
     }
     __syncthreads();
     // ---- B: masses of the entries [head, mark) in full passes (everything on the last step)
-    const int tail = s_tail;  // stable until the next selection
+    const int tail = *s_tail;  // stable until the next selection
     const int avail = (have ? mark : tail) - head;
     const int take = have ? avail / NT * NT : avail;
     mark = tail;
     for (int j = tid; j < take; j += NT) {
       const int slot = (head + j) & (CAP - 1);
-      const int64_t mo = s_mo[slot];
+      const int64_t mo = (int64_t)s_mo[slot] + mbase;
       T a[4], b[4];
       load_muon<T, AOS>(mu, mo, a);
       load_muon<T, AOS>(mu, mo + 1, b);
       const T M = event_mass<T, C_PTETAPHIM>(a, b);
       atomicAdd(&s_hist[find_bin(M, hp)], 1u);
-      if (WANT_M) m_out[s_ev[slot]] = M;
+      if (WANT_M) {
+        const uint32_t pe = s_ev[slot];
+        m_out[(blockIdx.x + (int64_t)(pe >> LOG2ET) * G) * ET + (pe & (ET - 1))] = M;
+      }
     }
     head += take;
     if (!have) break;
     __syncthreads();  // the slots consumed here may be refilled by the next selection
   }
+}
+
+// VOFF: offsets 32-byte aligned (full tiles take 256-bit offset loads).
+template <typename T, bool AOS, int ET, int NT, int MINB, bool WANT_M, bool VOFF>
+__global__ void __launch_bounds__(NT, MINB) k_dimuon_carry(View4<T> mu, const int32_t* __restrict__ q,
+                                                      const int64_t* __restrict__ offsets, int64_t n_events,
+                                                      HistParams hp, unsigned long long* __restrict__ bins,
+                                                      T* __restrict__ m_out) {
+  static_assert(DimuonCarry<ET / 2, NT>::CAP * (WANT_M ? 12 : 8) <= DimuonCarry<ET, NT>::CAP * (WANT_M ? 8 : 4),
+                "the 64-bit fallback list must fit the 32-bit list's bytes");
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem + (size_t)DimuonCarry<ET, NT>::CAP * 4 * (WANT_M ? 2 : 1));
+  __shared__ int s_tail;
+  const int nb2 = hp.nbins + 2;
+  for (int b = threadIdx.x; b < nb2; b += NT) s_hist[b] = 0u;
+  if (threadIdx.x == 0) s_tail = 0;
+  const int64_t first = __ldg(offsets), span = __ldg(offsets + n_events) - first;
+  if (span <= (int64_t)0xffffffffu)  // uniform over the grid
+    dimuon_carry_tiles<T, AOS, ET, NT, WANT_M, VOFF, uint32_t>(mu, q, offsets, n_events, hp, s_hist, smem, &s_tail,
+                                                               m_out, first);
+  else
+    dimuon_carry_tiles<T, AOS, ET / 2, NT, WANT_M, VOFF, int64_t>(mu, q, offsets, n_events, hp, s_hist, smem,
+                                                                  &s_tail, m_out, 0);
   __syncthreads();
-  for (int b = tid; b < nb2; b += NT) {
+  for (int b = threadIdx.x; b < nb2; b += NT) {
     const unsigned int c = s_hist[b];
     if (c) hist_flush(bins, hp, b, c);
   }

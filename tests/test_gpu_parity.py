@@ -632,6 +632,36 @@ def test_dimuon_carried_list_edges(gvx, O, dt):
     assert int(h.sum()) == 0 and bool(torch.isnan(m_out).all())
 
 
+def test_dimuon_muon_span_beyond_32_bits(gvx):
+    """k_dimuon_carry keeps 32-bit list entries (muon offset - offsets[0]) while a launch's
+    muons span < 2^32 and switches to 64-bit entries on half-size tiles otherwise. A first
+    event owning 2^32 + 7 muons (never selected: not two muons) pushes the span past 2^32;
+    the events after it must give the same bins and masses as the same events on their own
+    (which take the 32-bit path). f32, ~86 GB of muon columns (only the tail is written)."""
+    mu, q, off = synth.jagged_events(0, 100_003, seed=41, dtype=np.float32)
+    m = off[-1]
+    big = (1 << 32) + 7
+    free, _ = torch.cuda.mem_get_info()
+    need = (big + m) * (16 + 4) + (1 << 30)
+    if free < need:
+        pytest.skip(f"needs {need / 1e9:.0f} GB of free device memory")
+    ref_m = torch.empty(off.size - 1, dtype=torch.float32, device="cuda")
+    ref = host(gvx.dimuon_histogram(dev(mu), dev(q), dev(off), m_out=ref_m))
+    bm = torch.empty((big + m, 4), dtype=torch.float32, device="cuda")
+    bq = torch.empty(big + m, dtype=torch.int32, device="cuda")
+    bm[big:] = dev(mu)
+    bq[big:] = dev(q)
+    boff = torch.cat([torch.zeros(1, dtype=torch.int64, device="cuda"), dev(off) + big])
+    got_m = torch.empty(off.size, dtype=torch.float32, device="cuda")
+    got = host(gvx.dimuon_histogram(bm, bq, boff, m_out=got_m))
+    assert np.array_equal(got, ref)
+    assert bool(torch.isnan(got_m[0])) and torch.equal(torch.isnan(got_m[1:]), torch.isnan(ref_m))
+    ok = ~torch.isnan(ref_m)
+    assert torch.equal(got_m[1:][ok], ref_m[ok])
+    del bm, bq
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
 def test_lorentz_transform_parity(gvx, O, dt):
     v, beta = synth.boost_inputs(np.arange(200_003), dtype=dt, seed=23)

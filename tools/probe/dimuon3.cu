@@ -69,14 +69,14 @@ __device__ __forceinline__ void ld_offs(const int64_t* p, int64_t (&o)[EPT + 1])
 
 // PF bits: 1 prefetch the selected muon rows, 2 the offsets / charges of later tiles.
 // U: list entries per thread per mass pass (their gathers in flight together).
-template <typename T, int ET, int NT, int MINB, int PF, int CAP, int U = 1>
+template <typename T, int ET, int NT, int MINB, int PF, int CAP, int U = 1, typename LT = int64_t>
 __global__ void __launch_bounds__(NT, MINB) k_dimuon_pf(const T* __restrict__ mu, const int32_t* __restrict__ q,
                                                         const int64_t* __restrict__ offsets, int64_t n_events,
                                                         HistParams hp, unsigned long long* __restrict__ bins) {
   constexpr int EPT = ET / NT;
   static_assert((EPT % 4 == 0 && EPT <= 16) && (CAP & (CAP - 1)) == 0 && CAP >= 2 * ET + NT * U, "geometry");
   extern __shared__ __align__(16) unsigned char smem[];
-  int64_t* s_mo = reinterpret_cast<int64_t*>(smem);               // CAP muon offsets (circular)
+  LT* s_mo = reinterpret_cast<LT*>(smem);                         // CAP muon offsets (circular)
   unsigned int* s_hist = reinterpret_cast<unsigned int*>(s_mo + CAP);
   __shared__ int s_tail;
   const int nb2 = hp.nbins + 2;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_pf(const T* __restrict__ mu
 #pragma unroll
       for (int k = 0; k < EPT; ++k)
         if (mask & (1u << k)) {
-          s_mo[base++ & (CAP - 1)] = o[k];
+          s_mo[base++ & (CAP - 1)] = (LT)o[k];
           if (PF & 1) prefetch_l2(mu + 4 * o[k], 2 * RB);
         }
       if ((PF & 2) && tid == NT - 1) {  // the next tile's charges, the offsets two tiles ahead
@@ -266,9 +266,9 @@ void run(int64_t n) {
     View4<T> v{{mu, mu + 1, mu + 2, mu + 3}, 4};
     timeit([&] { kk<<<grid, 256, sm>>>(v, q, off, n, hp, bins, (T*)nullptr); }, "product k_dimuon_compact", ref);
   }
-  auto variant = [&](auto kk, int et, int cap, const char* name, int cps) {
+  auto variant = [&](auto kk, int et, int cap, const char* name, int cps, int esz) {
     const int nt = strstr(name, "NT128") ? 128 : strstr(name, "NT64") ? 64 : 256;
-    const size_t sm = (size_t)cap * 8 + 1002 * 4;
+    const size_t sm = (size_t)cap * esz + 1002 * 4;
     (void)et;
     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int sms = 0;
@@ -278,13 +278,16 @@ void run(int64_t n) {
     snprintf(buf, sizeof buf, "%s (grid %d)", name, grid);
     timeit([&] { kk<<<grid, nt, sm>>>(mu, q, off, n, hp, bins); }, buf, got);
   };
-  variant(k_dimuon_pf<T, 1024, 256, 4, 2, 4096, 1>, 1024, 4096, "pf2 ET1024 NT256 minb4 cps5 U1", 5);
-  variant(k_dimuon_pf<T, 1024, 256, 4, 6, 4096, 1>, 1024, 4096, "pf6 ET1024 NT256 minb4 cps5 U1", 5);
-  variant(k_dimuon_pf<T, 512, 128, 8, 2, 2048, 1>, 512, 2048, "pf2 ET512 NT128 minb8 cps8 U1", 8);
-  variant(k_dimuon_pf<T, 512, 128, 8, 6, 2048, 1>, 512, 2048, "pf6 ET512 NT128 minb8 cps8 U1", 8);
-  variant(k_dimuon_pf<T, 1024, 256, 4, 6, 4096, 1>, 1024, 4096, "pf6 ET1024 NT256 minb4 cps4 U1", 4);
-  variant(k_dimuon_pf<T, 512, 128, 6, 6, 2048, 1>, 512, 2048, "pf6 ET512 NT128 minb6 cps6 U1", 6);
-  variant(k_dimuon_pf<T, 512, 128, 8, 6, 2048, 2>, 512, 2048, "pf6 ET512 NT128 minb8 cps8 U2", 8);
+  variant(k_dimuon_pf<T, 512, 128, 8, 2, 2048, 1, int64_t>, 512, 2048, "pf2 ET512 NT128 minb8 cps8 int64_t", 8, sizeof(int64_t));
+  variant(k_dimuon_pf<T, 512, 128, 8, 2, 2048, 1, uint32_t>, 512, 2048, "pf2 ET512 NT128 minb8 cps8 uint32_t", 8, sizeof(uint32_t));
+  variant(k_dimuon_pf<T, 1024, 128, 8, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT128 minb8 cps8 uint32_t", 8, sizeof(uint32_t));
+  variant(k_dimuon_pf<T, 1024, 128, 6, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT128 minb6 cps6 uint32_t", 6, sizeof(uint32_t));
+  variant(k_dimuon_pf<T, 1024, 256, 4, 2, 4096, 1, int64_t>, 1024, 4096, "pf2 ET1024 NT256 minb4 cps5 int64_t", 5, sizeof(int64_t));
+  variant(k_dimuon_pf<T, 1024, 256, 4, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT256 minb4 cps5 uint32_t", 5, sizeof(uint32_t));
+  variant(k_dimuon_pf<T, 1024, 256, 4, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT256 minb4 cps6 uint32_t", 6, sizeof(uint32_t));
+  variant(k_dimuon_pf<T, 2048, 256, 4, 2, 8192, 1, uint32_t>, 2048, 8192, "pf2 ET2048 NT256 minb4 cps4 uint32_t", 4, sizeof(uint32_t));
+  variant(k_dimuon_pf<T, 512, 128, 10, 2, 2048, 1, uint32_t>, 512, 2048, "pf2 ET512 NT128 minb10 cps10 uint32_t", 10, sizeof(uint32_t));
+  variant(k_dimuon_pf<T, 1024, 128, 10, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT128 minb10 cps10 uint32_t", 10, sizeof(uint32_t));
   CK(cudaFree(k)); CK(cudaFree(off)); CK(cudaFree(tmp)); CK(cudaFree(mu)); CK(cudaFree(q)); CK(cudaFree(bins));
 }
 
