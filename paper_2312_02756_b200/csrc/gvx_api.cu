@@ -200,7 +200,7 @@ template <> struct TmaCfgOf<float, PM_HIST_CM> { using type = PairTma<float, 179
 template <> struct TmaCfgOf<float, PM_HIST_CM_COS> { using type = PairTma<float, 1792, 3, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_BOTH> { using type = PairTma<float, 1792, 3, 28, 1>; };
 
-#ifdef GVX_TUNE
+#if defined(GVX_TUNE) || defined(GVX_STEP_ALT)
 // Tuning build only (tools/libgvx_tune.so): GVX_TMA_CFG / GVX_LDG_CFG pick
 // alternative tile / ring / occupancy variants of the f64 kernels.
 int tune_env(const char* name) {
@@ -962,12 +962,85 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
     const double* pb = (const double*)beta->c[0];
     double* po = (double*)bout->c[0];
     gvx_status st;
-#ifdef GVX_TUNE
-    const int c = tune_env("GVX_STEP_CFG") ? tune_env("GVX_STEP_CFG") : 2;
-#else
-    const int c = 2;  // 18 pair warps + 6 boost warps (tools/step_probe.py: 2.62 vs 2.67-2.77 ms)
-#endif
-    if (c == 3)
+    // Default (round 2, session 3): 16 pair-consumer warps + 7 boost warps + 1 producer warp =
+    // 24 warps at 80 registers (25 warps were held to 72 and spilled 160 B), a 2-stage boost
+    // ring of 448-vector stages. Same-box sweep of 30 splits / ring shapes
+    // (profiles/r02/step_split_sweep.jsonl): 2.518 ms against 2.607 ms for round 1's 18 + 6
+    // warps with a 3 x 384 boost ring; 15 + 8 and 14 + 9 tie, 3- and 4-stage boost rings and
+    // one-vector-per-thread stages are slower.
+    using StepCfg = PairTma<double, 1024, 2, 16, 1>;
+    using StepBoost = BoostRing<double, 448, 2, 7>;
+#if defined(GVX_TUNE) || defined(GVX_STEP_ALT)
+    // Tuning builds: GVX_STEP_CFG picks another split (numbers as in the sweep file; unset or 0:
+    // the default; round 1's config 0 is 27 here).
+    const int c = tune_env("GVX_STEP_CFG");
+    if (c == 5)  // 17 pair + 6 boost + 1 producer warps: 24 warps, 80 registers
+      st = launch_step<double, PairTma<double, 1088, 2, 17, 1>, BoostRing<double, 384, 3, 6>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 6)  // 16 + 7 + 1
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 448, 3, 7>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 7)  // 18 + 5 + 1
+      st = launch_step<double, PairTma<double, 1152, 2, 18, 1>, BoostRing<double, 320, 3, 5>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 8)  // 17 + 6 + 1, 4-stage boost ring
+      st = launch_step<double, PairTma<double, 1088, 2, 17, 1>, BoostRing<double, 384, 4, 6>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 9)  // 17 + 6 + 1, 576-event boost stages
+      st = launch_step<double, PairTma<double, 1088, 2, 17, 1>, BoostRing<double, 576, 2, 6>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 10)  // 18 + 5 + 1, 480 x 2
+      st = launch_step<double, PairTma<double, 1152, 2, 18, 1>, BoostRing<double, 480, 2, 5>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 11)  // 18 + 5 + 1, 640 x 2
+      st = launch_step<double, PairTma<double, 1152, 2, 18, 1>, BoostRing<double, 640, 2, 5>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 12)  // 16 + 7 + 1, 672 x 2
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 672, 2, 7>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 13)  // 17 + 6 + 1, 384 x 2
+      st = launch_step<double, PairTma<double, 1088, 2, 17, 1>, BoostRing<double, 384, 2, 6>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 14)  // 18 + 6 + 1 (25 warps, 72 registers), 576 x 2
+      st = launch_step<double, PairTma<double, 1152, 2, 18, 1>, BoostRing<double, 576, 2, 6>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 15)  // 18 + 5 + 1, 320 x 2
+      st = launch_step<double, PairTma<double, 1152, 2, 18, 1>, BoostRing<double, 320, 2, 5>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 16)  // 16 + 7 + 1, 448 x 2
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 448, 2, 7>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 17)  // 17 + 6 + 1, 192 x 2
+      st = launch_step<double, PairTma<double, 1088, 2, 17, 1>, BoostRing<double, 192, 2, 6>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 18)  // 17 + 6 + 1, 192 x 4
+      st = launch_step<double, PairTma<double, 1088, 2, 17, 1>, BoostRing<double, 192, 4, 6>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 19)  // 20 + 3 + 1, 192 x 2
+      st = launch_step<double, PairTma<double, 1280, 2, 20, 1>, BoostRing<double, 192, 2, 3>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 20)  // 15 + 8 + 1, 512 x 2
+      st = launch_step<double, PairTma<double, 960, 2, 15, 1>, BoostRing<double, 512, 2, 8>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 21)  // 19 + 4 + 1, 256 x 2
+      st = launch_step<double, PairTma<double, 1216, 2, 19, 1>, BoostRing<double, 256, 2, 4>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 22)  // 14 + 9 + 1, 576 x 2
+      st = launch_step<double, PairTma<double, 896, 2, 14, 1>, BoostRing<double, 576, 2, 9>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 23)  // 16 + 7 + 1, 448 x 3
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 448, 3, 7>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 24)  // 15 + 8 + 1, 512 x 3
+      st = launch_step<double, PairTma<double, 960, 2, 15, 1>, BoostRing<double, 512, 3, 8>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 25)  // 16 + 7 + 1, 224 x 2
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 224, 2, 7>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 26)  // 15 + 8 + 1, 256 x 2
+      st = launch_step<double, PairTma<double, 960, 2, 15, 1>, BoostRing<double, 256, 2, 8>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 3)
       st = launch_step<double, PairTma<double, 1280, 2, 20, 1, 80>, BoostRing<double, 256, 4, 4, 80>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
     else if (c == 4)
@@ -976,12 +1049,19 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
     else if (c == 1)
       st = launch_step<double, PairTma<double, 1024, 2, 16, 1>, BoostRing<double, 512, 3, 8>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
-    else if (c == 0)
+    else if (c == 27)  // (round 1's config 0) 20 + 4 + 1, 256 x 4
       st = launch_step<double, PairTma<double, 1280, 2, 20, 1>, BoostRing<double, 256, 4, 4>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
-    else
+    else if (c == 2)  // round 1's default: 18 + 6 + 1 (25 warps, 72 registers), 384 x 3
       st = launch_step<double, PairTma<double, 1152, 2, 18, 1>, BoostRing<double, 384, 3, 6>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else
+      st = launch_step<double, StepCfg, StepBoost>(v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po,
+                                                   nb, s);
+#else
+    st = launch_step<double, StepCfg, StepBoost>(v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb,
+                                                 s);
+#endif
     if (st != GVX_ERR_UNSUPPORTED) return st;
   }
 #ifdef GVX_TUNE
