@@ -1064,8 +1064,8 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
 #endif
     if (st != GVX_ERR_UNSUPPORTED) return st;
   }
-#ifdef GVX_TUNE
-  // Tuning build only: the f32 step in one launch (GVX_STEP32_CFG = 1..4), for A/B runs.
+#if defined(GVX_TUNE) || defined(GVX_STEP_ALT)
+  // Tuning builds only: the f32 step in one launch (GVX_STEP32_CFG = 1..10), for A/B runs.
   const int c32 = tune_env("GVX_STEP32_CFG");
   if (c32 && dtype == GVX_F32 && n >= (int64_t(1) << 20) && nb >= (int64_t(1) << 20) && coords == GVX_PTETAPHIM &&
       tma_enabled() && classify(v1, es) == L_AOS && classify(v2, es) == L_AOS && aos4(bv, es) &&
@@ -1086,6 +1086,27 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
     else if (c32 == 4)
       st = launch_step<float, PairTma<float, 1280, 3, 20, 1, 72>, BoostRing<float, 768, 3, 8, 56>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 5)  // 16 + 7 + 1 (24 warps, 80 registers), pair 1024 x 3, boost 448 x 2
+      st = launch_step<float, PairTma<float, 1024, 3, 16, 1>, BoostRing<float, 448, 2, 7>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 6)  // 16 + 7 + 1, pair 2048 x 3, boost 448 x 2
+      st = launch_step<float, PairTma<float, 2048, 3, 16, 1>, BoostRing<float, 448, 2, 7>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 7)  // 15 + 8 + 1, pair 960 x 4, boost 512 x 2
+      st = launch_step<float, PairTma<float, 960, 4, 15, 1>, BoostRing<float, 512, 2, 8>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 8)  // 18 + 5 + 1, pair 1152 x 3, boost 320 x 2
+      st = launch_step<float, PairTma<float, 1152, 3, 18, 1>, BoostRing<float, 320, 2, 5>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 9)  // 16 + 7 + 1, pair 1024 x 4, boost 448 x 2
+      st = launch_step<float, PairTma<float, 1024, 4, 16, 1>, BoostRing<float, 448, 2, 7>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 10)  // 14 + 9 + 1, pair 896 x 4, boost 576 x 2
+      st = launch_step<float, PairTma<float, 896, 4, 14, 1>, BoostRing<float, 576, 2, 9>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c32 == 11)  // 20 + 3 + 1, pair 1280 x 3, boost 192 x 2
+      st = launch_step<float, PairTma<float, 1280, 3, 20, 1>, BoostRing<float, 192, 2, 3>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
     if (st != GVX_ERR_UNSUPPORTED) return st;
   }
