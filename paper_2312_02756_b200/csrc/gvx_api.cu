@@ -1040,6 +1040,15 @@ gvx_status gvx_pair_histograms_boost(gvx_dtype dtype, gvx_coords coords, const g
     else if (c == 26)  // 15 + 8 + 1, 256 x 2
       st = launch_step<double, PairTma<double, 960, 2, 15, 1>, BoostRing<double, 256, 2, 8>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 28)  // setmaxnreg: 16 pair at 96 + 8 boost at 48 + 4-warp producer at 24, boost 512 x 2
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1, 96>, BoostRing<double, 512, 2, 8, 48>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 29)  // setmaxnreg: 16 pair at 88 + 8 boost at 64, boost 512 x 2
+      st = launch_step<double, PairTma<double, 1024, 2, 16, 1, 88>, BoostRing<double, 512, 2, 8, 64>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
+    else if (c == 30)  // setmaxnreg: 20 pair at 80 + 4 boost at 80, boost 256 x 2
+      st = launch_step<double, PairTma<double, 1280, 2, 20, 1, 80>, BoostRing<double, 256, 2, 4, 80>>(
+          v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
     else if (c == 3)
       st = launch_step<double, PairTma<double, 1280, 2, 20, 1, 80>, BoostRing<double, 256, 4, 4, 80>>(
           v1, v2, n, hp, lab_bins, cm_bins, m_out, cm_m_out, pv, pb, po, nb, s);
