@@ -189,11 +189,14 @@ template <typename T, int MODE> struct TmaCfgOf;
 template <int MODE> struct TmaCfgOf<double, MODE> { using type = PairTma<double, 896, 2, 28, 1>; };
 // fp64 CM: 24 consumer warps x 2 events each, run as two interleaved chains
 // (pair_consume_x2): 1.16 vs 1.24 ms for 31 warps x 1 event
-// (profiles/r01/sweep_f64_cm_x2.jsonl).
-template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 1536, 2, 24, 1>; };
+// (profiles/r01/sweep_f64_cm_x2.jsonl). Since round 2 (session 3) with the fused pass's
+// setmaxnreg split (4-warp producer at 24 registers, consumers at 80): CM histogram
+// 1.14-1.16 -> 1.12-1.13 ms, peaked CM histogram 1.20-1.26 -> 1.17-1.22 ms (same-box A/B,
+// profiles/r02/cm_creg_ab.jsonl).
+template <> struct TmaCfgOf<double, PM_HIST_CM> { using type = PairTma<double, 1536, 2, 24, 1, 80>; };
 // fp64 lab histogram: 20 warps x 2 interleaved events, 0.904 vs 0.934 ms (same sweep)
 template <> struct TmaCfgOf<double, PM_HIST> { using type = PairTma<double, 1280, 2, 20, 1>; };
-template <> struct TmaCfgOf<double, PM_HIST_CM_COS> { using type = PairTma<double, 1536, 2, 24, 1>; };
+template <> struct TmaCfgOf<double, PM_HIST_CM_COS> { using type = PairTma<double, 1536, 2, 24, 1, 80>; };
 template <> struct TmaCfgOf<double, PM_BOTH> { using type = PairTma<double, 1536, 2, 24, 1, 80>; };
 template <int MODE> struct TmaCfgOf<float, MODE> { using type = PairTma<float, 896, 4, 28, 1>; };
 template <> struct TmaCfgOf<float, PM_HIST_CM> { using type = PairTma<float, 1792, 3, 28, 1>; };
