@@ -203,6 +203,131 @@ __global__ void __launch_bounds__(NT, MINB) k_dimuon_pf(const T* __restrict__ mu
   }
 }
 
+
+// Warp-specialised variant: NS selection warps feed NM mass warps through the circular
+// list with no CTA-wide barrier (selection warps sync among themselves with a named
+// barrier per tile and publish the list tail; mass warps claim 32 entries at a time).
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+template <typename T, int ET, int NS, int NM, int CAP, int MINB>
+__global__ void __launch_bounds__(32 * (NS + NM), MINB) k_dimuon_ws(const T* __restrict__ mu, const int32_t* __restrict__ q,
+                                                              const int64_t* __restrict__ offsets, int64_t n_events,
+                                                              HistParams hp, unsigned long long* __restrict__ bins) {
+  constexpr int NST = NS * 32, EPT = ET / NST;
+  static_assert(ET % NST == 0 && EPT % 4 == 0 && (CAP & (CAP - 1)) == 0 && CAP >= 2 * ET + 64 * NM, "geometry");
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* s_mo = reinterpret_cast<uint32_t*>(smem);
+  unsigned int* s_hist = reinterpret_cast<unsigned int*>(s_mo + CAP);
+  __shared__ int s_reserve, s_claim;
+  __shared__ volatile int s_tail, s_done;
+  __shared__ volatile int s_pos[NM];
+  const int nb2 = hp.nbins + 2;
+  for (int b = threadIdx.x; b < nb2; b += blockDim.x) s_hist[b] = 0u;
+  if (threadIdx.x == 0) { s_reserve = 0; s_claim = 0; s_tail = 0; s_done = 0; }
+  if (threadIdx.x < NM) s_pos[threadIdx.x] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t first = __ldg(offsets);
+  const int64_t ntiles = (n_events + ET - 1) / ET;
+  const int64_t G = gridDim.x;
+  auto tile_events = [&](int64_t t) { return n_events - t * ET < ET ? n_events - t * ET : (int64_t)ET; };
+  if (warp < NS) {
+    const int tid = threadIdx.x;
+    if (tid == 0)
+      for (int64_t t = blockIdx.x; t < ntiles && t < blockIdx.x + 2 * G; t += G)
+        prefetch_range((const char*)(offsets + t * ET), (const char*)(offsets + t * ET + tile_events(t) + 1));
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += G) {
+      const int64_t e0 = tile * ET;
+      const int ne = (int)tile_events(tile);
+      const int lb = tid * EPT;
+      int64_t o[EPT + 1];
+      if (ne == ET) {
+        ld_offs<EPT>(offsets + e0 + lb, o);
+      } else {
+#pragma unroll
+        for (int k = 0; k <= EPT; ++k) o[k] = lb + k <= ne ? __ldg(offsets + e0 + lb + k) : 0;
+      }
+      int32_t qa[EPT], qb[EPT];
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        qa[k] = qb[k] = 0;
+        if (lb + k < ne && o[k + 1] - o[k] == 2) {
+          qa[k] = __ldg(q + o[k]);
+          qb[k] = __ldg(q + o[k] + 1);
+        }
+      }
+      unsigned int mask = 0u;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k)
+        mask |= (unsigned int)(((qa[k] ^ qb[k]) < 0) & (qa[k] != 0) & (qb[k] != 0)) << k;
+      const int cnt = __popc(mask);
+      int incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      int base = 0;
+      if (lane == 31 && incl) {
+        base = atomicAdd(&s_reserve, incl);
+        // capacity: the oldest entry still held by a mass warp must stay CAP - ET behind
+        for (;;) {
+          int mn = s_pos[0];
+#pragma unroll
+          for (int w = 1; w < NM; ++w) mn = min(mn, (int)s_pos[w]);
+          if (base + incl - mn <= CAP) break;
+          __nanosleep(64);
+        }
+      }
+      base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k)
+        if (mask & (1u << k)) s_mo[base++ & (CAP - 1)] = (uint32_t)(o[k] - first);
+      __threadfence_block();
+      named_sync(1, NST);
+      if (tid == 0) {
+        s_tail = s_reserve;
+        const int64_t t1 = tile + G, t2 = tile + 2 * G;
+        if (t1 < ntiles) prefetch_range((const char*)(q + __ldg(offsets + t1 * ET)), (const char*)(q + __ldg(offsets + t1 * ET + tile_events(t1))));
+        if (t2 < ntiles) prefetch_range((const char*)(offsets + t2 * ET), (const char*)(offsets + t2 * ET + tile_events(t2) + 1));
+      }
+    }
+    named_sync(1, NST);
+    if (threadIdx.x == 0) {
+      __threadfence_block();
+      s_done = 1;
+    }
+  } else {
+    const int mw = warp - NS;
+    for (;;) {
+      int c = 0;
+      if (lane == 0) {
+        c = atomicAdd(&s_claim, 32);
+        s_pos[mw] = c;
+        while (s_tail < c + 32 && !s_done) __nanosleep(32);
+      }
+      c = __shfl_sync(0xffffffffu, c, 0);
+      __threadfence_block();
+      const int tail = s_tail;  // >= c + 32, or final (producers done)
+      if (c >= tail) break;
+      const int j = c + lane;
+      if (j < tail) {
+        const int64_t oo = (int64_t)s_mo[j & (CAP - 1)] + first;
+        T a[4], b[4];
+        ld_gather(mu + 4 * oo, a);
+        ld_gather(mu + 4 * oo + 4, b);
+        const T M = event_mass<T, C_PTETAPHIM>(a, b);
+        atomicAdd(&s_hist[find_bin(M, hp)], 1u);
+      }
+    }
+    if (lane == 0) s_pos[mw] = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
+    const unsigned int c = s_hist[b];
+    if (c) atomicAdd(&bins[b], (unsigned long long)c);
+  }
+}
+
 template <typename K>
 int resident(K k, int block, size_t smem) {
   int per = 0, sms = 0;
@@ -266,6 +391,16 @@ void run(int64_t n) {
     View4<T> v{{mu, mu + 1, mu + 2, mu + 3}, 4};
     timeit([&] { kk<<<grid, 256, sm>>>(v, q, off, n, hp, bins, (T*)nullptr); }, "product k_dimuon_compact", ref);
   }
+  auto wsvar = [&](auto kk, int et, int cap, int nt, const char* name, int cps) {
+    const size_t sm = (size_t)cap * 4 + 1002 * 4;
+    CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int grid = std::min<int64_t>(std::min(resident(kk, nt, sm), cps * sms), (n + et - 1) / et);
+    char buf[128];
+    snprintf(buf, sizeof buf, "%s (grid %d)", name, grid);
+    timeit([&] { kk<<<grid, nt, sm>>>(mu, q, off, n, hp, bins); }, buf, got);
+  };
   auto variant = [&](auto kk, int et, int cap, const char* name, int cps, int esz) {
     const int nt = strstr(name, "NT128") ? 128 : strstr(name, "NT64") ? 64 : 256;
     const size_t sm = (size_t)cap * esz + 1002 * 4;
@@ -278,16 +413,14 @@ void run(int64_t n) {
     snprintf(buf, sizeof buf, "%s (grid %d)", name, grid);
     timeit([&] { kk<<<grid, nt, sm>>>(mu, q, off, n, hp, bins); }, buf, got);
   };
-  variant(k_dimuon_pf<T, 512, 128, 8, 2, 2048, 1, int64_t>, 512, 2048, "pf2 ET512 NT128 minb8 cps8 int64_t", 8, sizeof(int64_t));
-  variant(k_dimuon_pf<T, 512, 128, 8, 2, 2048, 1, uint32_t>, 512, 2048, "pf2 ET512 NT128 minb8 cps8 uint32_t", 8, sizeof(uint32_t));
-  variant(k_dimuon_pf<T, 1024, 128, 8, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT128 minb8 cps8 uint32_t", 8, sizeof(uint32_t));
-  variant(k_dimuon_pf<T, 1024, 128, 6, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT128 minb6 cps6 uint32_t", 6, sizeof(uint32_t));
-  variant(k_dimuon_pf<T, 1024, 256, 4, 2, 4096, 1, int64_t>, 1024, 4096, "pf2 ET1024 NT256 minb4 cps5 int64_t", 5, sizeof(int64_t));
-  variant(k_dimuon_pf<T, 1024, 256, 4, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT256 minb4 cps5 uint32_t", 5, sizeof(uint32_t));
-  variant(k_dimuon_pf<T, 1024, 256, 4, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT256 minb4 cps6 uint32_t", 6, sizeof(uint32_t));
-  variant(k_dimuon_pf<T, 2048, 256, 4, 2, 8192, 1, uint32_t>, 2048, 8192, "pf2 ET2048 NT256 minb4 cps4 uint32_t", 4, sizeof(uint32_t));
-  variant(k_dimuon_pf<T, 512, 128, 10, 2, 2048, 1, uint32_t>, 512, 2048, "pf2 ET512 NT128 minb10 cps10 uint32_t", 10, sizeof(uint32_t));
-  variant(k_dimuon_pf<T, 1024, 128, 10, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT128 minb10 cps10 uint32_t", 10, sizeof(uint32_t));
+  variant(k_dimuon_pf<T, 1024, 128, 8, 2, 4096, 1, uint32_t>, 1024, 4096, "pf2 ET1024 NT128 minb8 cps8 uint32_t", 8, 4);
+  variant(k_dimuon_pf<T, 2048, 256, 4, 2, 8192, 1, uint32_t>, 2048, 8192, "pf2 ET2048 NT256 minb4 cps4 uint32_t", 4, 4);
+  wsvar(k_dimuon_ws<T, 1024, 4, 4, 4096, 4>, 1024, 4096, 256, "ws ET1024 4+4 cps4", 4);
+  wsvar(k_dimuon_ws<T, 1024, 4, 4, 4096, 6>, 1024, 4096, 256, "ws ET1024 4+4 cps6", 6);
+  wsvar(k_dimuon_ws<T, 512, 2, 2, 2048, 8>, 512, 2048, 128, "ws ET512 2+2 cps8", 8);
+  wsvar(k_dimuon_ws<T, 512, 2, 4, 2048, 6>, 512, 2048, 192, "ws ET512 2+4 cps6", 6);
+  wsvar(k_dimuon_ws<T, 1024, 4, 8, 4096, 4>, 1024, 4096, 384, "ws ET1024 4+8 cps4", 4);
+  wsvar(k_dimuon_ws<T, 2048, 8, 8, 8192, 2>, 2048, 8192, 512, "ws ET2048 8+8 cps2", 2);
   CK(cudaFree(k)); CK(cudaFree(off)); CK(cudaFree(tmp)); CK(cudaFree(mu)); CK(cudaFree(q)); CK(cudaFree(bins));
 }
 
