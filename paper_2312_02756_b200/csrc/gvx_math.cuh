@@ -503,10 +503,25 @@ __device__ __forceinline__ T cm_pair_mass(const V4<T>& a, const V4<T>& b, V4<T>*
   // A_Y0: a.y is exactly zero, so P_y = b.y (0 + b.y differs at most in the sign of a zero)
   T Px = a.x + b.x, Py = A_Y0 ? b.y : a.y + b.y, Pz = a.z + b.z, E = a.t + b.t;
   T inv = any_rcp(E);
-  BoostCoef<T> k = boost_coef_fast(-Px * inv, -Py * inv, -Pz * inv);
-  const bool ok = k.ok && is_positive(E);
-  k.g = ok ? k.g : T(NAN);
-  k.bg = ok ? k.bg : T(NAN);
+  BoostCoef<T> k;
+  if constexpr (sizeof(T) == 8) {
+    // boost_coef_fast's arithmetic with the validity folded into u = 1 - beta^2: E <= 0 (or
+    // -NaN) selects a NaN u, and beta^2 >= 1 gives u <= 0, whose MUFU.RSQ64H seed is NaN
+    // (-0 and flushed denormals give inf, whose refinement is NaN) — one double select
+    // instead of a validity test and two (g, bg) selects; the same values, NaN -> NaN.
+    k.bx = -Px * inv;
+    k.by = -Py * inv;
+    k.bz = -Pz * inv;
+    double u = 1.0 - (k.bx * k.bx + k.by * k.by + k.bz * k.bz);
+    u = is_positive(E) ? u : __longlong_as_double(0x7ff8000000000000ll);
+    k.g = fast_rsqrt(u);
+    k.bg = fast_rcp(fma(u, k.g, u));
+  } else {
+    k = boost_coef_fast(-Px * inv, -Py * inv, -Pz * inv);
+    const bool ok = k.ok && is_positive(E);
+    k.g = ok ? k.g : T(NAN);
+    k.bg = ok ? k.bg : T(NAN);
+  }
   k.ok = true;
   V4<T> a2 = apply_boost<T, A_Y0>(k, a), b2 = apply_boost(k, b);
   if (a_out) { *a_out = a2; *b_out = b2; }
